@@ -1,0 +1,141 @@
+/*
+ * rs_poly.h -- C ABI of the B200-native polynomial Reed-Solomon library.
+ *
+ * The operations are those of Sheykh Esmaili & Datta, "On the Effectiveness of
+ * Polynomial Realization of Reed-Solomon Codes for Storage Systems" (arXiv
+ * 1312.5155, PAPER.md; "P:n" = PAPER.md line n):
+ *   - RS(k,m) over GF(2^w): k data elements are encoded into n = k+m so that any
+ *     k of the n recover the object.
+ *   - generator polynomial g(x) = prod_{i=0}^{m-1} (x + alpha^i), alpha = 2
+ *     (P:170-177);
+ *   - encode: parity p(x) = d(x) x^m mod g(x) (Eq. 1-2);
+ *   - decode: Step 1 evaluates the survivors at alpha^0..alpha^{t-1}, Step 2
+ *     solves the t x t Vandermonde system for the t erased symbols
+ *     (P:213-303).  Results are bit-identical to the literal definitions.
+ *
+ * Layout and conventions:
+ *   - A stripe holds n blocks of block_bytes bytes each.  API block index
+ *     b in [0,n): 0..k-1 are data, k..n-1 are parity.
+ *   - Column c of a stripe = symbol c of every block; each column is an
+ *     independent codeword.  Data block j is the coefficient of x^{m+j}
+ *     (P:191), parity block i the coefficient of x^i.
+ *   - w = 8: one byte per symbol.  w = 16: little-endian uint16 per symbol, so
+ *     block_bytes must be even.
+ *   - "Device pointer" = CUDA global memory of the current device (e.g. a
+ *     torch.cuda tensor's data_ptr()).  Streams are cudaStream_t passed as
+ *     void* (NULL = legacy default stream).
+ *
+ * Ownership: the caller owns every block buffer and stream.  A plan owns its
+ * host tables and its decode-pattern cache (mutex-guarded); a plan may be used
+ * from several host threads and streams at once.
+ *
+ * Errors are returned synchronously after argument validation and before any
+ * device work; on a validation error nothing is written.  Launch failures
+ * return RS_ERR_CUDA; asynchronous device faults surface at stream sync.
+ * There is no CPU fallback: every entry point that computes runs CUDA kernels.
+ */
+#ifndef RS_POLY_H
+#define RS_POLY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_POLY_ABI_VERSION 1
+#define RS_POLY_MAX_N 255 /* k+m <= 255 (also k+m <= 2^w-1, reading G7) */
+#define RS_POLY_MAX_M 32
+
+typedef struct rs_poly_plan rs_poly_plan; /* opaque */
+
+typedef enum {
+  RS_OK = 0,
+  RS_ERR_INVALID_ARG = 1,       /* null pointer, k<1, m<1, m>RS_POLY_MAX_M, w not 8/16, k+m > min(255, 2^w-1) */
+  RS_ERR_NOT_PRIMITIVE = 2,     /* prim_poly not of degree w, or ord(alpha=2) != 2^w-1              */
+  RS_ERR_GEOMETRY = 3,          /* block_bytes == 0, block_bytes % (w/8) != 0, pointer/stride not w/8-aligned */
+  RS_ERR_TOO_MANY_ERASURES = 4, /* |E| > m: the code recovers at most m erasures                  */
+  RS_ERR_BAD_ERASURE = 5,       /* erasure index outside [0,n) or listed twice                              */
+  RS_ERR_CUDA = 6,              /* a CUDA runtime call or kernel launch failed                               */
+  RS_ERR_NOMEM = 7              /* host or device allocation failed                                          */
+} rs_status;
+
+/* ---- plan ------------------------------------------------------------------
+ * Builds, on the host: exp/log of GF(2^w) from prim_poly with alpha = 2,
+ * g(x), the k x m parity map (column j = x^{m+j} mod g, the
+ * generator-matrix form of g) and the kernels' packed constants.
+ * No device memory is touched; constants reach the device as kernel
+ * parameters / per-call uploads.  *out receives the plan, or NULL on error. */
+rs_status rs_poly_plan_create(int k, int m, int w, uint32_t prim_poly, rs_poly_plan **out);
+void rs_poly_plan_destroy(rs_poly_plan *plan); /* NULL is a no-op */
+
+/* g_out[0..m] receives g low->high (monic); pmap_out[i*k + j] (m x k,
+ * row = parity i, column = data j) the parity map P with p_i = sum_j P[i][j] d_j.
+ * Either pointer may be NULL.  Host memory.  Host-only (no GPU needed). */
+rs_status rs_poly_plan_info(const rs_poly_plan *plan, uint32_t *g_out, uint32_t *pmap_out);
+
+/* Which kernel family the plan uses: 1 = bit-sliced XOR network specialised at
+ * compile time for this (k,m,w,prim_poly); 0 = generic split-nibble tables.   */
+int rs_poly_plan_kernel_kind(const rs_poly_plan *plan);
+
+/* ---- single stripe (pointer arrays) ---------------------------------------
+ * data:   HOST array of k DEVICE pointers (read only).
+ * parity: HOST array of m DEVICE pointers (overwritten with p_0..p_{m-1}).
+ * Encode: all-zero data gives all-zero parity. */
+rs_status rs_poly_encode(const rs_poly_plan *plan, const void *const *data, void *const *parity,
+                         size_t block_bytes, void *stream);
+
+/* blocks: HOST array of n DEVICE pointers, data 0..k-1 then parity k..n-1.
+ * erasures: HOST array of n_erasures API block indices, any order, 0 <= n_erasures <= m.
+ * Decode: writes the original bytes into exactly the erased blocks
+ * (their prior contents are don't-care) and never writes a survivor.
+ * n_erasures == 0 is a successful no-op. */
+rs_status rs_poly_decode(const rs_poly_plan *plan, void *const *blocks, size_t block_bytes,
+                         const int *erasures, int n_erasures, void *stream);
+
+/* ---- batched, strided layout ------------------------------------------------
+ * Block b of stripe s lives at stripes + s*stripe_stride + b*block_stride
+ * (bytes; DEVICE memory).  The usual layout is [S][n][B]: block_stride = B,
+ * stripe_stride = n*B.  Strides must be multiples of w/8.
+ * Encode writes blocks k..n-1 of every stripe. */
+rs_status rs_poly_encode_batch(const rs_poly_plan *plan, void *stripes, size_t n_stripes,
+                               size_t stripe_stride, size_t block_stride, size_t block_bytes, void *stream);
+
+/* erasures: HOST int32 [n_stripes][m], row s lists stripe s's erased API block
+ * indices padded with -1 (each stripe may have its own pattern; an all -1 row
+ * leaves that stripe untouched).  The per-pattern decode constants (the
+ * paper's Opt1/Opt3: alpha powers and the inverted Vandermonde
+ * matrix, computed once per pattern) are cached in the plan. */
+rs_status rs_poly_decode_batch(const rs_poly_plan *plan, void *stripes, size_t n_stripes,
+                               size_t stripe_stride, size_t block_stride, size_t block_bytes,
+                               const int32_t *erasures, void *stream);
+
+/* ---- end to end from HOST memory ---------------------------------------------
+ * Same operations, but `host_stripes` is HOST memory (page-locked for full
+ * speed, e.g. cudaHostAlloc / torch pin_memory), laid out as in the batched
+ * calls.  The library streams chunks of stripes through device staging
+ * buffers it allocates on `stream`'s device: host->device copy of the inputs
+ * (encode: the k data blocks; decode: the n-t survivors), the kernel, and the
+ * device->host copy of the outputs (encode: m parity blocks; decode: the t
+ * erased blocks), overlapped across chunks.  Returns after the results are in
+ * host memory.  *h2d_bytes / *d2h_bytes (optional) receive the bytes copied. */
+rs_status rs_poly_encode_host(const rs_poly_plan *plan, void *host_stripes, size_t n_stripes,
+                              size_t stripe_stride, size_t block_stride, size_t block_bytes,
+                              void *stream, uint64_t *h2d_bytes, uint64_t *d2h_bytes);
+rs_status rs_poly_decode_host(const rs_poly_plan *plan, void *host_stripes, size_t n_stripes,
+                              size_t stripe_stride, size_t block_stride, size_t block_bytes,
+                              const int32_t *erasures, void *stream, uint64_t *h2d_bytes,
+                              uint64_t *d2h_bytes);
+
+/* ---- misc ----------------------------------------------------------------- */
+const char *rs_poly_strerror(rs_status status);
+int rs_poly_abi_version(void);
+
+/* Kernels launched by this library since load (all entry points, all threads). */
+uint64_t rs_poly_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RS_POLY_H */

@@ -1,0 +1,610 @@
+// plan.cpp -- host planner, decode-pattern cache and C ABI (include/rs_poly.h).
+//
+// Plan creation: field tables, g(x), parity map.
+// Decode patterns (P:213-303 with the paper's Opt1-Opt3): for an
+// erasure set E (t = |E| <= m) the planner builds, once per pattern,
+//   V_E[j][e]  = (alpha^{pos_e})^j, j < t          (Step-2 Vandermonde matrix)
+//   V_E^{-1}                                          (Opt3: inverted once)
+//   W = V_E^{-1} H_par[0:t,:],  H_par[j][i] = alpha^{j i}   (bit-sliced path)
+//   R = V_E^{-1} A_E,  A_E[j][s] = alpha^{j pos(s)} over survivors s (generic)
+// and the packed split-nibble tables the kernels read.  Both are exact
+// rewritings of y = V_E^{-1} (D(alpha^0..alpha^{t-1})) -- see DESIGN.md.
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/rs_poly.h"
+#include "gf.hpp"
+#include "rs_kernels.cuh"
+
+using rsb::Field;
+
+namespace {
+
+struct PatternHost {
+  std::vector<int> erased;  // row order of W / R: ascending API index
+  rsb::SlicedPat sp{};
+  std::vector<uint8_t> wtab;  // sliced W tables
+  rsb::GenericPat gp{};
+  std::vector<uint8_t> rtab;  // generic R tables (all output groups)
+};
+
+using MaskKey = std::array<uint64_t, 4>;
+
+}  // namespace
+
+struct rs_poly_plan {
+  int k = 0, m = 0, w = 0, n = 0;
+  uint32_t poly = 0;
+  Field F;
+  std::vector<uint32_t> g, pmap;
+  bool sliced = false;
+  rsb::GenericPat enc_gp{};
+  std::vector<uint8_t> enc_tab;
+  mutable std::mutex mu;
+  mutable std::map<MaskKey, std::shared_ptr<const PatternHost>> cache;
+};
+
+namespace {
+
+constexpr int kGenericThreads = 256;
+constexpr int kSlicedThreads = 128;
+constexpr uint32_t kSlicedUnitsPerCta = kSlicedThreads * 8;
+constexpr uint64_t kGenericChunk = 64 * 1024;
+
+// Packed split-nibble tables for "out_r = sum_s M[r][s] in_s" (layout in rs_kernels.cuh).
+void pack_generic_tables(const Field &F, int w, const std::vector<uint32_t> &M, int n_out, int n_in,
+                         std::vector<uint8_t> &out) {
+  const int groups = (n_out + 3) / 4;
+  const int nh = w / 4;               // nibbles per symbol
+  const size_t eb = (w == 8) ? 4 : 8;  // entry bytes
+  out.assign((size_t)groups * n_in * nh * 16 * eb, 0);
+  for (int g = 0; g < groups; ++g)
+    for (int s = 0; s < n_in; ++s)
+      for (int h = 0; h < nh; ++h)
+        for (uint32_t v = 0; v < 16; ++v) {
+          uint64_t packed = 0;
+          for (int r = 0; r < 4 && 4 * g + r < n_out; ++r) {
+            uint64_t prod = F.mul(M[(size_t)(4 * g + r) * n_in + s], v << (4 * h));
+            packed |= prod << (w * r);
+          }
+          uint8_t *dst = out.data() + ((((size_t)g * n_in + s) * nh + h) * 16 + v) * eb;
+          std::memcpy(dst, &packed, eb);  // little-endian host
+        }
+}
+
+std::shared_ptr<const PatternHost> build_pattern(const rs_poly_plan &P, const std::vector<int> &er) {
+  const Field &F = P.F;
+  const int t = (int)er.size(), k = P.k, m = P.m, n = P.n;
+  auto ph = std::make_shared<PatternHost>();
+  ph->erased = er;
+  // Opt1: alpha powers of the erased positions; Step-2 matrix
+  std::vector<uint32_t> V((size_t)t * t), X(t);
+  for (int e = 0; e < t; ++e) X[e] = F.alpha_pow((uint64_t)rsb::position(er[e], k, m));
+  for (int j = 0; j < t; ++j)
+    for (int e = 0; e < t; ++e) V[(size_t)j * t + e] = F.alpha_pow((uint64_t)F.log_[X[e]] * (uint64_t)j);
+  if (!rsb::invert(F, V, t)) return nullptr;  // Opt3: V^{-1} once per pattern
+  // W = V^{-1} H_par[0:t, :]  (t x m)
+  std::vector<uint32_t> W((size_t)t * m, 0);
+  for (int e = 0; e < t; ++e)
+    for (int i = 0; i < m; ++i) {
+      uint32_t acc = 0;
+      for (int j = 0; j < t; ++j) acc ^= F.mul(V[(size_t)e * t + j], F.alpha_pow((uint64_t)j * (uint64_t)i));
+      W[(size_t)e * m + i] = acc;
+    }
+  // R = V^{-1} A_E over the survivors (t x (n-t))
+  std::vector<int> surv;
+  std::vector<char> is_er(n, 0);
+  for (int b : er) is_er[b] = 1;
+  for (int b = 0; b < n; ++b)
+    if (!is_er[b]) surv.push_back(b);
+  const int ns = (int)surv.size();
+  std::vector<uint32_t> R((size_t)t * ns, 0);
+  for (int e = 0; e < t; ++e)
+    for (int si = 0; si < ns; ++si) {
+      uint32_t acc = 0;
+      const uint64_t p = (uint64_t)rsb::position(surv[si], k, m);
+      for (int j = 0; j < t; ++j) acc ^= F.mul(V[(size_t)e * t + j], F.alpha_pow((uint64_t)j * p));
+      R[(size_t)e * ns + si] = acc;
+    }
+  // sliced record
+  if (P.sliced) {
+    std::memset(&ph->sp, 0, sizeof(ph->sp));
+    for (int b : er) ph->sp.erased_mask[b >> 5] |= 1u << (b & 31);
+    ph->sp.t = t;
+    for (int e = 0; e < t && e < 4; ++e) ph->sp.out_blk[e] = (uint8_t)er[e];
+    pack_generic_tables(F, P.w, W, t, m, ph->wtab);  // one group (t <= 4): [i][h][v]
+  }
+  // generic record
+  std::memset(&ph->gp, 0, sizeof(ph->gp));
+  ph->gp.n_in = ns;
+  ph->gp.n_out = t;
+  for (int si = 0; si < ns; ++si) ph->gp.in_blk[si] = (uint8_t)surv[si];
+  for (int e = 0; e < t; ++e) ph->gp.out_blk[e] = (uint8_t)er[e];
+  pack_generic_tables(F, P.w, R, t, ns, ph->rtab);
+  return ph;
+}
+
+rs_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return RS_OK;
+  if (e == cudaErrorMemoryAllocation) return RS_ERR_NOMEM;
+  return RS_ERR_CUDA;
+}
+
+// Per-call device blob: uploaded with one H2D copy, freed stream-ordered.
+struct Blob {
+  std::vector<uint8_t> h;
+  size_t add(const void *p, size_t bytes) {
+    size_t off = (h.size() + 15) & ~(size_t)15;
+    h.resize(off + bytes);
+    if (p && bytes) std::memcpy(h.data() + off, p, bytes);
+    return off;
+  }
+};
+
+struct Geometry {
+  rsb::Layout L{};
+  uint64_t n_stripes = 0, block_bytes = 0;
+  bool aligned32 = false, aligned16 = false;
+};
+
+bool ptr_aligned(uint64_t v, uint64_t a) { return (v % a) == 0; }
+
+// Launch encode (pats==nullptr) or decode over a geometry whose constants are in dev blob.
+struct LaunchPlan {
+  // offsets into the device blob
+  size_t pat_idx_off = SIZE_MAX, sliced_pats_off = SIZE_MAX, generic_pats_off = SIZE_MAX, ptrs_off = SIZE_MAX;
+  size_t tables_off = 0;
+  uint32_t generic_groups = 1, generic_smem = 0;
+};
+
+rs_status run_kernels(const rs_poly_plan &P, bool decode, Geometry G, const LaunchPlan &lp, uint8_t *dev,
+                      cudaStream_t st) {
+  if (lp.ptrs_off != SIZE_MAX) G.L.ptrs = reinterpret_cast<const uint64_t *>(dev + lp.ptrs_off);
+  const uint64_t UB = 32ull * (uint64_t)P.w / 8;
+  uint64_t body_units = 0;
+  if (P.sliced && G.aligned32) body_units = G.block_bytes / UB;
+  if (body_units) {
+    rsb::SlicedArgs a{};
+    a.L = G.L;
+    a.n_stripes = G.n_stripes;
+    a.units_per_stripe = body_units;
+    a.units_per_cta = kSlicedUnitsPerCta;
+    a.ctas_per_stripe = (uint32_t)((body_units + kSlicedUnitsPerCta - 1) / kSlicedUnitsPerCta);
+    if (decode) {
+      a.pats = reinterpret_cast<const rsb::SlicedPat *>(dev + lp.sliced_pats_off);
+      a.pat_idx = reinterpret_cast<const int32_t *>(dev + lp.pat_idx_off);
+      a.tables = dev + lp.tables_off;
+    }
+    cudaError_t e = rsb::launch_sliced(P.k, P.m, P.w, P.poly, decode, a, st);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  const uint64_t col_begin = body_units * UB;
+  if (col_begin < G.block_bytes) {
+    rsb::GenericArgs a{};
+    a.L = G.L;
+    a.pats = reinterpret_cast<const rsb::GenericPat *>(dev + lp.generic_pats_off);
+    a.pat_idx = lp.pat_idx_off == SIZE_MAX ? nullptr : reinterpret_cast<const int32_t *>(dev + lp.pat_idx_off);
+    a.tables = dev + lp.tables_off;
+    a.n_stripes = G.n_stripes;
+    a.col_begin = col_begin;
+    a.col_end = G.block_bytes;
+    const uint64_t span = G.block_bytes - col_begin;
+    const uint64_t step = (uint64_t)kGenericThreads * 16;
+    uint64_t chunk = std::min<uint64_t>(kGenericChunk, (span + step - 1) / step * step);
+    a.chunk_bytes = chunk;
+    a.ctas_per_group = (uint32_t)((span + chunk - 1) / chunk);
+    a.n_groups = lp.generic_groups;
+    a.vec_ok = G.aligned16 ? 1u : 0u;
+    a.smem_bytes = lp.generic_smem;
+    cudaError_t e = rsb::launch_generic(P.w, a, st);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  return RS_OK;
+}
+
+// Upload a blob and run; the blob is freed stream-ordered after the kernels.
+rs_status upload_and_run(const rs_poly_plan &P, bool decode, const Geometry &G, const LaunchPlan &lp, Blob &b,
+                         cudaStream_t st) {
+  void *dev = nullptr;
+  cudaError_t e = cudaMallocAsync(&dev, std::max<size_t>(b.h.size(), 16), st);
+  if (e != cudaSuccess) return cuda_status(e);
+  e = cudaMemcpyAsync(dev, b.h.data(), b.h.size(), cudaMemcpyHostToDevice, st);
+  rs_status rc = e == cudaSuccess ? run_kernels(P, decode, G, lp, static_cast<uint8_t *>(dev), st) : cuda_status(e);
+  cudaError_t ef = cudaFreeAsync(dev, st);
+  if (rc == RS_OK && ef != cudaSuccess) rc = cuda_status(ef);
+  return rc;
+}
+
+rs_status check_geometry(const rs_poly_plan *P, size_t block_bytes) {
+  if (!P) return RS_ERR_INVALID_ARG;
+  if (block_bytes == 0 || block_bytes % (size_t)(P->w / 8)) return RS_ERR_GEOMETRY;
+  return RS_OK;
+}
+
+rs_status encode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs, cudaStream_t st) {
+  Blob b;
+  LaunchPlan lp;
+  if (ptrs) lp.ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
+  lp.generic_pats_off = b.add(&P->enc_gp, sizeof(P->enc_gp));
+  lp.tables_off = b.add(P->enc_tab.data(), P->enc_tab.size());
+  rsb::GenericPat gp = P->enc_gp;
+  gp.table_off = 0;
+  std::memcpy(b.h.data() + lp.generic_pats_off, &gp, sizeof(gp));
+  lp.generic_groups = (uint32_t)((P->m + 3) / 4);
+  lp.generic_smem = (uint32_t)(P->k * (P->w == 8 ? 128 : 512));
+  return upload_and_run(*P, false, G, lp, b, st);
+}
+
+// rows: per stripe list of erased API indices (validated, sorted ascending)
+rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
+                      const std::vector<std::vector<int>> &rows, cudaStream_t st) {
+  // distinct patterns
+  std::vector<std::shared_ptr<const PatternHost>> pats;
+  std::map<MaskKey, int> local;
+  std::vector<int32_t> idx(G.n_stripes, -1);
+  bool any = false;
+  {
+    std::lock_guard<std::mutex> lock(P->mu);
+    for (uint64_t s = 0; s < G.n_stripes; ++s) {
+      const auto &er = rows[s];
+      if (er.empty()) continue;
+      MaskKey key{0, 0, 0, 0};
+      for (int b : er) key[b >> 6] |= 1ull << (b & 63);
+      auto it = local.find(key);
+      if (it != local.end()) { idx[s] = it->second; any = true; continue; }
+      auto c = P->cache.find(key);
+      std::shared_ptr<const PatternHost> ph;
+      if (c != P->cache.end()) {
+        ph = c->second;
+      } else {
+        ph = build_pattern(*P, er);
+        if (!ph) return RS_ERR_INVALID_ARG;
+        P->cache.emplace(key, ph);
+      }
+      idx[s] = (int)pats.size();
+      local.emplace(key, (int)pats.size());
+      pats.push_back(ph);
+      any = true;
+    }
+  }
+  if (!any) return RS_OK;
+  Blob b;
+  LaunchPlan lp;
+  if (ptrs) lp.ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
+  lp.pat_idx_off = b.add(idx.data(), sizeof(int32_t) * idx.size());
+  std::vector<rsb::SlicedPat> sps(pats.size());
+  std::vector<rsb::GenericPat> gps(pats.size());
+  lp.sliced_pats_off = b.add(nullptr, sizeof(rsb::SlicedPat) * sps.size());
+  lp.generic_pats_off = b.add(nullptr, sizeof(rsb::GenericPat) * gps.size());
+  lp.tables_off = b.add(nullptr, 0);
+  uint32_t max_groups = 1, max_in = 1;
+  for (size_t i = 0; i < pats.size(); ++i) {
+    const PatternHost &ph = *pats[i];
+    if (P->sliced) {
+      sps[i] = ph.sp;
+      sps[i].table_off = (uint32_t)(b.add(ph.wtab.data(), ph.wtab.size()) - lp.tables_off);
+    }
+    gps[i] = ph.gp;
+    gps[i].table_off = (uint32_t)(b.add(ph.rtab.data(), ph.rtab.size()) - lp.tables_off);
+    max_groups = std::max<uint32_t>(max_groups, (uint32_t)((ph.gp.n_out + 3) / 4));
+    max_in = std::max<uint32_t>(max_in, (uint32_t)ph.gp.n_in);
+  }
+  std::memcpy(b.h.data() + lp.sliced_pats_off, sps.data(), sizeof(rsb::SlicedPat) * sps.size());
+  std::memcpy(b.h.data() + lp.generic_pats_off, gps.data(), sizeof(rsb::GenericPat) * gps.size());
+  lp.generic_groups = max_groups;
+  lp.generic_smem = max_in * (P->w == 8 ? 128 : 512);
+  return upload_and_run(*P, true, G, lp, b, st);
+}
+
+rs_status parse_row(const rs_poly_plan *P, const int32_t *row, int count, std::vector<int> &out, bool allow_pad) {
+  out.clear();
+  std::vector<char> seen(P->n, 0);
+  for (int i = 0; i < count; ++i) {
+    int b = row[i];
+    if (allow_pad && b == -1) continue;
+    if (b < 0 || b >= P->n) return RS_ERR_BAD_ERASURE;
+    if (seen[b]) return RS_ERR_BAD_ERASURE;
+    seen[b] = 1;
+    out.push_back(b);
+  }
+  if ((int)out.size() > P->m) return RS_ERR_TOO_MANY_ERASURES;
+  std::sort(out.begin(), out.end());
+  return RS_OK;
+}
+
+Geometry strided(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t ss, size_t bs, size_t B) {
+  Geometry G;
+  G.L.base = static_cast<uint8_t *>(stripes);
+  G.L.stripe_stride = ss;
+  G.L.block_stride = bs;
+  G.L.n = P->n;
+  G.n_stripes = n_stripes;
+  G.block_bytes = B;
+  const uint64_t base = reinterpret_cast<uint64_t>(stripes);
+  G.aligned32 = ptr_aligned(base, 32) && ptr_aligned(ss, 32) && ptr_aligned(bs, 32);
+  G.aligned16 = ptr_aligned(base, 16) && ptr_aligned(ss, 16) && ptr_aligned(bs, 16);
+  return G;
+}
+
+rs_status check_strided(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t ss, size_t bs, size_t B) {
+  rs_status rc = check_geometry(P, B);
+  if (rc) return rc;
+  if (n_stripes && !stripes) return RS_ERR_INVALID_ARG;
+  const uint64_t a = (uint64_t)(P->w / 8);
+  if (!ptr_aligned(reinterpret_cast<uint64_t>(stripes), a) || ss % a || bs % a) return RS_ERR_GEOMETRY;
+  if (P->n > 1 && bs < B) return RS_ERR_GEOMETRY;                      // blocks overlap
+  if (n_stripes > 1 && ss < (uint64_t)(P->n - 1) * bs + B) return RS_ERR_GEOMETRY;  // stripes overlap
+  return RS_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int rs_poly_abi_version(void) { return RS_POLY_ABI_VERSION; }
+uint64_t rs_poly_launch_count(void) { return rsb::launches_total(); }
+
+const char *rs_poly_strerror(rs_status s) {
+  switch (s) {
+    case RS_OK: return "ok";
+    case RS_ERR_INVALID_ARG: return "invalid argument";
+    case RS_ERR_NOT_PRIMITIVE: return "prim_poly is not a primitive polynomial of degree w with alpha=2";
+    case RS_ERR_GEOMETRY: return "bad block geometry (size/alignment)";
+    case RS_ERR_TOO_MANY_ERASURES: return "more than m erasures";
+    case RS_ERR_BAD_ERASURE: return "erasure index out of range or duplicated";
+    case RS_ERR_CUDA: return "CUDA error";
+    case RS_ERR_NOMEM: return "out of memory";
+  }
+  return "unknown status";
+}
+
+rs_status rs_poly_plan_create(int k, int m, int w, uint32_t prim_poly, rs_poly_plan **out) {
+  if (!out) return RS_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (k < 1 || m < 1 || m > RS_POLY_MAX_M || (w != 8 && w != 16)) return RS_ERR_INVALID_ARG;
+  const int n = k + m;
+  if (n > RS_POLY_MAX_N || (uint32_t)n > (1u << w) - 1) return RS_ERR_INVALID_ARG;
+  auto *P = new (std::nothrow) rs_poly_plan();
+  if (!P) return RS_ERR_NOMEM;
+  if (!P->F.init(w, prim_poly)) {
+    delete P;
+    return RS_ERR_NOT_PRIMITIVE;
+  }
+  P->k = k; P->m = m; P->w = w; P->n = n; P->poly = prim_poly;
+  P->g = rsb::generator_poly(P->F, m);
+  P->pmap = rsb::parity_map(P->F, k, m, P->g);
+  P->sliced = rsb::sliced_available(k, m, w, prim_poly);
+  std::memset(&P->enc_gp, 0, sizeof(P->enc_gp));
+  P->enc_gp.n_in = k;
+  P->enc_gp.n_out = m;
+  for (int j = 0; j < k; ++j) P->enc_gp.in_blk[j] = (uint8_t)j;
+  for (int i = 0; i < m; ++i) P->enc_gp.out_blk[i] = (uint8_t)(k + i);
+  pack_generic_tables(P->F, w, P->pmap, m, k, P->enc_tab);
+  *out = P;
+  return RS_OK;
+}
+
+void rs_poly_plan_destroy(rs_poly_plan *plan) { delete plan; }
+
+rs_status rs_poly_plan_info(const rs_poly_plan *P, uint32_t *g_out, uint32_t *pmap_out) {
+  if (!P) return RS_ERR_INVALID_ARG;
+  if (g_out) std::memcpy(g_out, P->g.data(), sizeof(uint32_t) * P->g.size());
+  if (pmap_out) std::memcpy(pmap_out, P->pmap.data(), sizeof(uint32_t) * P->pmap.size());
+  return RS_OK;
+}
+
+int rs_poly_plan_kernel_kind(const rs_poly_plan *P) { return P && P->sliced ? 1 : 0; }
+
+rs_status rs_poly_encode(const rs_poly_plan *P, const void *const *data, void *const *parity, size_t block_bytes,
+                         void *stream) {
+  rs_status rc = check_geometry(P, block_bytes);
+  if (rc) return rc;
+  if (!data || !parity) return RS_ERR_INVALID_ARG;
+  std::vector<uint64_t> ptrs(P->n);
+  bool a32 = true, a16 = true;
+  const uint64_t sa = (uint64_t)(P->w / 8);
+  for (int b = 0; b < P->n; ++b) {
+    const void *p = b < P->k ? data[b] : parity[b - P->k];
+    if (!p) return RS_ERR_INVALID_ARG;
+    ptrs[b] = reinterpret_cast<uint64_t>(p);
+    if (ptrs[b] % sa) return RS_ERR_GEOMETRY;
+    a32 = a32 && ptr_aligned(ptrs[b], 32);
+    a16 = a16 && ptr_aligned(ptrs[b], 16);
+  }
+  Geometry G;
+  G.L.n = P->n;
+  G.n_stripes = 1;
+  G.block_bytes = block_bytes;
+  G.aligned32 = a32;
+  G.aligned16 = a16;
+  return encode_impl(P, G, ptrs.data(), static_cast<cudaStream_t>(stream));
+}
+
+rs_status rs_poly_decode(const rs_poly_plan *P, void *const *blocks, size_t block_bytes, const int *erasures,
+                         int n_erasures, void *stream) {
+  rs_status rc = check_geometry(P, block_bytes);
+  if (rc) return rc;
+  if (!blocks || n_erasures < 0 || (n_erasures > 0 && !erasures)) return RS_ERR_INVALID_ARG;
+  if (n_erasures > P->m) return RS_ERR_TOO_MANY_ERASURES;
+  std::vector<std::vector<int>> rows(1);
+  std::vector<int32_t> row(erasures, erasures + n_erasures);
+  rc = parse_row(P, row.data(), n_erasures, rows[0], false);
+  if (rc) return rc;
+  if (rows[0].empty()) return RS_OK;
+  std::vector<uint64_t> ptrs(P->n);
+  bool a32 = true, a16 = true;
+  const uint64_t sa = (uint64_t)(P->w / 8);
+  for (int b = 0; b < P->n; ++b) {
+    if (!blocks[b]) return RS_ERR_INVALID_ARG;
+    ptrs[b] = reinterpret_cast<uint64_t>(blocks[b]);
+    if (ptrs[b] % sa) return RS_ERR_GEOMETRY;
+    a32 = a32 && ptr_aligned(ptrs[b], 32);
+    a16 = a16 && ptr_aligned(ptrs[b], 16);
+  }
+  Geometry G;
+  G.L.n = P->n;
+  G.n_stripes = 1;
+  G.block_bytes = block_bytes;
+  G.aligned32 = a32;
+  G.aligned16 = a16;
+  return decode_impl(P, G, ptrs.data(), rows, static_cast<cudaStream_t>(stream));
+}
+
+rs_status rs_poly_encode_batch(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
+                               size_t block_stride, size_t block_bytes, void *stream) {
+  rs_status rc = check_strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
+  if (rc) return rc;
+  if (n_stripes == 0) return RS_OK;
+  Geometry G = strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
+  return encode_impl(P, G, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+rs_status rs_poly_decode_batch(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
+                               size_t block_stride, size_t block_bytes, const int32_t *erasures, void *stream) {
+  rs_status rc = check_strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
+  if (rc) return rc;
+  if (n_stripes == 0) return RS_OK;
+  if (!erasures) return RS_ERR_INVALID_ARG;
+  std::vector<std::vector<int>> rows(n_stripes);
+  for (size_t s = 0; s < n_stripes; ++s) {
+    rc = parse_row(P, erasures + s * (size_t)P->m, P->m, rows[s], true);
+    if (rc) return rc;
+  }
+  Geometry G = strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
+  return decode_impl(P, G, nullptr, rows, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// End to end from host memory: chunks of stripes stream through device
+// staging buffers, H2D -> kernels -> D2H, overlapped over kNumLanes streams.
+// ===========================================================================
+namespace {
+
+constexpr int kNumLanes = 3;
+constexpr uint64_t kStagingTarget = 256ull << 20;  // bytes of staging per lane
+
+rs_status host_impl(const rs_poly_plan *P, bool decode, uint8_t *host, size_t n_stripes, size_t ss, size_t bs,
+                    size_t B, const int32_t *erasures, cudaStream_t user, uint64_t *h2d, uint64_t *d2h) {
+  rs_status rc = check_strided(P, host, n_stripes, ss, bs, B);
+  if (rc) return rc;
+  std::vector<std::vector<int>> rows;
+  if (decode) {
+    if (!erasures) return RS_ERR_INVALID_ARG;
+    rows.resize(n_stripes);
+    for (size_t s = 0; s < n_stripes; ++s) {
+      rc = parse_row(P, erasures + s * (size_t)P->m, P->m, rows[s], true);
+      if (rc) return rc;
+    }
+  }
+  uint64_t in_bytes = 0, out_bytes = 0;
+  if (n_stripes == 0) {
+    if (h2d) *h2d = 0;
+    if (d2h) *d2h = 0;
+    return RS_OK;
+  }
+  const int n = P->n;
+  const uint64_t Bp = (B + 255) & ~255ull;  // device block pitch (32-byte aligned for the sliced path)
+  const uint64_t stripe_dev = Bp * (uint64_t)n;
+  const uint64_t per_chunk = std::max<uint64_t>(1, kStagingTarget / stripe_dev);
+  cudaStream_t lanes[kNumLanes] = {};
+  uint8_t *stage[kNumLanes] = {};
+  cudaEvent_t start = nullptr;
+  cudaError_t e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(start, user);
+  for (int l = 0; l < kNumLanes && e == cudaSuccess; ++l) {
+    e = cudaStreamCreateWithFlags(&lanes[l], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(lanes[l], start, 0);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void **>(&stage[l]), per_chunk * stripe_dev, lanes[l]);
+  }
+  rc = cuda_status(e);
+  for (size_t s0 = 0, ci = 0; rc == RS_OK && s0 < n_stripes; s0 += per_chunk, ++ci) {
+    const size_t cnt = std::min<size_t>(per_chunk, n_stripes - s0);
+    const int l = (int)(ci % kNumLanes);
+    cudaStream_t st = lanes[l];
+    // inputs host -> device
+    for (size_t s = s0; s < s0 + cnt && e == cudaSuccess; ++s) {
+      uint8_t *hs = host + s * ss, *ds = stage[l] + (s - s0) * stripe_dev;
+      if (!decode) {
+        e = cudaMemcpy2DAsync(ds, Bp, hs, bs, B, (size_t)P->k, cudaMemcpyHostToDevice, st);
+        in_bytes += (uint64_t)P->k * B;
+      } else {
+        std::vector<char> er(n, 0);
+        for (int b : rows[s]) er[b] = 1;
+        if (rows[s].empty()) continue;
+        for (int b = 0; b < n && e == cudaSuccess; ++b)
+          if (!er[b]) {
+            e = cudaMemcpyAsync(ds + b * Bp, hs + b * bs, B, cudaMemcpyHostToDevice, st);
+            in_bytes += B;
+          }
+      }
+    }
+    if (e != cudaSuccess) { rc = cuda_status(e); break; }
+    Geometry G = strided(P, stage[l], cnt, stripe_dev, Bp, B);
+    if (!decode) {
+      rc = encode_impl(P, G, nullptr, st);
+    } else {
+      std::vector<std::vector<int>> sub(rows.begin() + s0, rows.begin() + s0 + cnt);
+      rc = decode_impl(P, G, nullptr, sub, st);
+    }
+    if (rc) break;
+    // outputs device -> host
+    for (size_t s = s0; s < s0 + cnt && e == cudaSuccess; ++s) {
+      uint8_t *hs = host + s * ss, *ds = stage[l] + (s - s0) * stripe_dev;
+      if (!decode) {
+        e = cudaMemcpy2DAsync(hs + (size_t)P->k * bs, bs, ds + (size_t)P->k * Bp, Bp, B, (size_t)P->m,
+                              cudaMemcpyDeviceToHost, st);
+        out_bytes += (uint64_t)P->m * B;
+      } else {
+        for (int b : rows[s]) {
+          if (e != cudaSuccess) break;
+          e = cudaMemcpyAsync(hs + b * bs, ds + b * Bp, B, cudaMemcpyDeviceToHost, st);
+          out_bytes += B;
+        }
+      }
+    }
+    if (e != cudaSuccess) rc = cuda_status(e);
+  }
+  for (int l = 0; l < kNumLanes; ++l) {
+    if (stage[l]) cudaFreeAsync(stage[l], lanes[l]);
+    if (lanes[l]) {
+      cudaError_t es = cudaStreamSynchronize(lanes[l]);
+      if (rc == RS_OK && es != cudaSuccess) rc = cuda_status(es);
+      cudaStreamDestroy(lanes[l]);
+    }
+  }
+  if (start) cudaEventDestroy(start);
+  if (h2d) *h2d = in_bytes;
+  if (d2h) *d2h = out_bytes;
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+rs_status rs_poly_encode_host(const rs_poly_plan *P, void *host_stripes, size_t n_stripes, size_t stripe_stride,
+                              size_t block_stride, size_t block_bytes, void *stream, uint64_t *h2d_bytes,
+                              uint64_t *d2h_bytes) {
+  return host_impl(P, false, static_cast<uint8_t *>(host_stripes), n_stripes, stripe_stride, block_stride,
+                   block_bytes, nullptr, static_cast<cudaStream_t>(stream), h2d_bytes, d2h_bytes);
+}
+
+rs_status rs_poly_decode_host(const rs_poly_plan *P, void *host_stripes, size_t n_stripes, size_t stripe_stride,
+                              size_t block_stride, size_t block_bytes, const int32_t *erasures, void *stream,
+                              uint64_t *h2d_bytes, uint64_t *d2h_bytes) {
+  return host_impl(P, true, static_cast<uint8_t *>(host_stripes), n_stripes, stripe_stride, block_stride,
+                   block_bytes, erasures, static_cast<cudaStream_t>(stream), h2d_bytes, d2h_bytes);
+}
+
+}  // extern "C"

@@ -1,0 +1,465 @@
+// rs_kernels.cu -- sm_100a kernels of the polynomial Reed-Solomon hot path.
+//
+// What they compute (PAPER.md, arXiv 1312.5155):
+//   encode: parity p(x) = d(x) x^m mod g(x), g = prod_{i<m}(x + alpha^i)
+//           (Eq. 1-2), per column of each stripe;
+//   decode: the erased symbols of each column from the survivors (two-step
+//           decode).
+//
+// Two kernel families:
+//   * sliced_kernel<K,M,W,POLY,DECODE>: each thread owns 32 columns; it loads
+//     32*W/8 bytes of each block with 256-bit loads, transposes them into W
+//     bit-planes (three/four delta swaps), applies the compile-time GF(2)
+//     network RsNet (parity map of g, P:459 + bit-matrix form) and
+//     transposes back.  Decode re-encodes the surviving data (erased data
+//     zeroed), XORs the received parity to get Delta = H_par^{-1}-side
+//     residue, and solves the t erased symbols with the runtime t x m matrix
+//     W = V_E^{-1} H_par[0:t,:] through split-nibble tables in shared memory.
+//   * generic_kernel<W>: out_r = sum_s M[r][s] in_s with runtime split-nibble
+//     tables (any k, m, any erasure pattern, any alignment, ragged tails).
+// Every HBM byte of a stripe is read once or written once: (k+m)*B per pass.
+#include <atomic>
+#include <cstdio>
+
+#include "rs_kernels.cuh"
+#include "rs_networks.cuh"
+
+namespace rsb {
+
+static std::atomic<uint64_t> g_launches{0};
+uint64_t launches_total() { return g_launches.load(); }
+void count_launch() { g_launches.fetch_add(1); }
+
+// ---------------------------------------------------------------------------
+// memory helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ldg_v4(const void *p) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg_v4(void *p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void ldg_v8(const void *p, uint32_t *r) {
+  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void stg_v8(void *p, const uint32_t *r) {
+  asm volatile("st.global.L1::no_allocate.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+                  "r"(r[7])
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// bit-plane transposes (delta swaps; each is an involution, so the same
+// routine goes bytes -> planes and planes -> bytes)
+// ---------------------------------------------------------------------------
+// Left shift on the FMA pipe (IMAD.SHL), right shift on the ALU pipe (SHF):
+// the ALU pipe (64 lanes/clk/SM on B200) is the scarce one.
+template <int S>
+__device__ __forceinline__ uint32_t shl_fma(uint32_t v) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(v), "n"(1u << S));
+  return r;
+}
+
+// Swap in-word bit S-position (mask ~M) of a with word-index bit of c.
+template <int S, uint32_t MASK>
+__device__ __forceinline__ void delta_swap(uint32_t &a, uint32_t &c) {
+  const uint32_t cs = shl_fma<S>(c);
+  const uint32_t as = a >> S;
+  const uint32_t na = (a & MASK) | (cs & ~MASK);
+  const uint32_t nc = (as & MASK) | (c & ~MASK);
+  a = na;
+  c = nc;
+}
+
+// 8 words (32 columns of bytes; word i = columns 4i..4i+3) <-> 8 planes
+// (plane b = bit b of the 32 columns; column 4i+r at plane bit 8r+i).
+__device__ __forceinline__ void transpose8(uint32_t *x) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) delta_swap<4, 0x0F0F0F0Fu>(x[i], x[i + 4]);
+#pragma unroll
+  for (int i = 0; i < 8; i += 4) {
+    delta_swap<2, 0x33333333u>(x[i], x[i + 2]);
+    delta_swap<2, 0x33333333u>(x[i + 1], x[i + 3]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) delta_swap<1, 0x55555555u>(x[i], x[i + 1]);
+}
+
+// 16 words (32 columns of LE uint16; word i = columns 2i, 2i+1) <-> 16 planes
+// (plane b = bit b; column 2i+r at plane bit 16r+i).  The byte stage uses PRMT.
+__device__ __forceinline__ void transpose16(uint32_t *x) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t a = x[i], c = x[i + 8];
+    x[i] = __byte_perm(a, c, 0x6240);
+    x[i + 8] = __byte_perm(a, c, 0x7351);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if ((i & 4) == 0) delta_swap<4, 0x0F0F0F0Fu>(x[i], x[i + 4]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if ((i & 2) == 0) delta_swap<2, 0x33333333u>(x[i], x[i + 2]);
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) delta_swap<1, 0x55555555u>(x[i], x[i + 1]);
+}
+
+template <int W>
+__device__ __forceinline__ void transposeW(uint32_t *x) {
+  if (W == 8) transpose8(x);
+  else transpose16(x);
+}
+
+template <int W>
+__device__ __forceinline__ void load_unit(const uint8_t *p, uint32_t *x) {
+  ldg_v8(p, x);
+  if (W == 16) ldg_v8(p + 32, x + 8);
+}
+template <int W>
+__device__ __forceinline__ void store_unit(uint8_t *p, const uint32_t *x) {
+  stg_v8(p, x);
+  if (W == 16) stg_v8(p + 32, x + 8);
+}
+
+// Load + transpose the data blocks of CSE group G and run its sub-network
+// (group 0 assigns y, later groups accumulate).  Erased data blocks (decode)
+// are not read: their planes are zero.
+template <int K, int M, int W, uint32_t POLY, bool DECODE, int G>
+__device__ __forceinline__ void net_groups(uint8_t *const *blk, uint64_t off, uint32_t emask,
+                                           uint32_t (&y)[M * W]) {
+  using Grp = RsNetGroup<K, M, W, POLY, G>;
+  constexpr int J0 = Grp::kFirstBlock, NB = Grp::kBlocks;
+  uint32_t x[NB * W];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    if (DECODE && ((emask >> (J0 + j)) & 1u)) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) x[j * W + q] = 0;
+    } else {
+      load_unit<W>(blk[J0 + j] + off, &x[j * W]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) transposeW<W>(&x[j * W]);
+  Grp::run(x, y);
+  if constexpr (G + 1 < RsNet<K, M, W, POLY>::kGroups)
+    net_groups<K, M, W, POLY, DECODE, G + 1>(blk, off, emask, y);
+}
+
+// ---------------------------------------------------------------------------
+// bit-sliced kernel
+// ---------------------------------------------------------------------------
+template <int K, int M, int W, uint32_t POLY, bool DECODE>
+__global__ void __launch_bounds__(128) sliced_kernel(const SlicedArgs a) {
+  constexpr int UB = 32 * W / 8;                    // bytes per unit per block
+  constexpr int TAB_WORDS = M * (W / 4) * 16 * (W / 8);  // W-step tables, 32-bit words
+  __shared__ __align__(16) uint32_t wtab[DECODE ? TAB_WORDS : 1];
+
+  const uint64_t s = blockIdx.x / a.ctas_per_stripe;
+  const uint32_t c = blockIdx.x % a.ctas_per_stripe;
+  if (s >= a.n_stripes) return;
+
+  uint32_t emask = 0;
+  int t = 0;
+  uint8_t outb[4] = {0, 0, 0, 0};
+  if (DECODE) {
+    const int pi = a.pat_idx[s];
+    if (pi < 0) return;
+    const SlicedPat &P = a.pats[pi];
+    emask = P.erased_mask[0];
+    t = P.t;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) outb[e] = P.out_blk[e];
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.tables + P.table_off);
+    for (int i = threadIdx.x; i < TAB_WORDS / 4; i += blockDim.x) reinterpret_cast<uint4 *>(wtab)[i] = src[i];
+    __syncthreads();
+  }
+
+  uint8_t *blk[K + M];
+#pragma unroll
+  for (int b = 0; b < K + M; ++b) blk[b] = a.L.block(s, b);
+
+  const uint64_t u0 = (uint64_t)c * a.units_per_cta;
+  const uint64_t u1 = min(u0 + a.units_per_cta, a.units_per_stripe);
+  for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+    const uint64_t off = u * UB;
+    uint32_t y[M * W];
+    net_groups<K, M, W, POLY, DECODE, 0>(blk, off, emask, y);
+#pragma unroll
+    for (int i = 0; i < M; ++i) transposeW<W>(&y[i * W]);
+
+    if (!DECODE) {
+#pragma unroll
+      for (int i = 0; i < M; ++i) store_unit<W>(blk[K + i] + off, &y[i * W]);
+      continue;
+    }
+
+    // Delta_i = received parity_i ^ encode(surviving data)_i (erased parity: received = 0)
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      if (!((emask >> (K + i)) & 1u)) {
+        uint32_t r[W];
+        load_unit<W>(blk[K + i] + off, r);
+#pragma unroll
+        for (int q = 0; q < W; ++q) y[i * W + q] ^= r[q];
+      }
+    }
+
+    if (W == 8) {
+      // y_e = sum_i W[e][i] Delta_i, four erasures packed per 32-bit table word.
+      uint32_t acc[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q] = 0;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const char *Tl = reinterpret_cast<const char *>(&wtab[i * 32]);
+        const char *Th = reinterpret_cast<const char *>(&wtab[i * 32 + 16]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t v = y[i * W + q];
+          const uint32_t lo = shl_fma<2>(v) & 0x3C3C3C3Cu;  // low nibbles * 4 (byte offsets)
+          const uint32_t hi = (v >> 2) & 0x3C3C3C3Cu;       // high nibbles * 4
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const uint32_t il = (lo >> (8 * r)) & 0xFFu, ih = (hi >> (8 * r)) & 0xFFu;
+            acc[4 * q + r] ^= *reinterpret_cast<const uint32_t *>(Tl + il) ^
+                              *reinterpret_cast<const uint32_t *>(Th + ih);
+          }
+        }
+      }
+      // 4x4 byte transposes: acc[4q+r] byte e -> output e, word q, byte r
+      uint32_t o[4][8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t t0 = __byte_perm(acc[4 * q], acc[4 * q + 1], 0x5140);
+        const uint32_t t1 = __byte_perm(acc[4 * q], acc[4 * q + 1], 0x7362);
+        const uint32_t t2 = __byte_perm(acc[4 * q + 2], acc[4 * q + 3], 0x5140);
+        const uint32_t t3 = __byte_perm(acc[4 * q + 2], acc[4 * q + 3], 0x7362);
+        o[0][q] = __byte_perm(t0, t2, 0x5410);
+        o[1][q] = __byte_perm(t0, t2, 0x7632);
+        o[2][q] = __byte_perm(t1, t3, 0x5410);
+        o[3][q] = __byte_perm(t1, t3, 0x7632);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < t) store_unit<W>(a.L.block(s, outb[e]) + off, o[e]);
+    } else {
+      // w = 16: entries are 4 x 16-bit lanes (uint2), four nibbles per symbol.
+      uint2 acc[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q] = make_uint2(0, 0);
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const char *T0 = reinterpret_cast<const char *>(&wtab[i * 128]);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const uint32_t v = y[i * W + q];
+          const uint32_t lo = shl_fma<3>(v) & 0x78787878u;  // nibbles 0,2 of both symbols * 8
+          const uint32_t hi = (v >> 1) & 0x78787878u;       // nibbles 1,3 * 8
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {  // symbol r of the word = column 2q+r
+            const uint32_t n0 = (lo >> (16 * r)) & 0xFFu, n2 = (lo >> (16 * r + 8)) & 0xFFu;
+            const uint32_t n1 = (hi >> (16 * r)) & 0xFFu, n3 = (hi >> (16 * r + 8)) & 0xFFu;
+            const uint2 e0 = *reinterpret_cast<const uint2 *>(T0 + 0 * 128 + n0);
+            const uint2 e1 = *reinterpret_cast<const uint2 *>(T0 + 1 * 128 + n1);
+            const uint2 e2 = *reinterpret_cast<const uint2 *>(T0 + 2 * 128 + n2);
+            const uint2 e3 = *reinterpret_cast<const uint2 *>(T0 + 3 * 128 + n3);
+            acc[2 * q + r].x ^= e0.x ^ e1.x ^ e2.x ^ e3.x;
+            acc[2 * q + r].y ^= e0.y ^ e1.y ^ e2.y ^ e3.y;
+          }
+        }
+      }
+      uint32_t o[16];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (e < t) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const uint32_t a0 = (e < 2) ? acc[2 * q].x : acc[2 * q].y;
+            const uint32_t a1 = (e < 2) ? acc[2 * q + 1].x : acc[2 * q + 1].y;
+            o[q] = __byte_perm(a0, a1, (e & 1) ? 0x7632 : 0x5410);
+          }
+          store_unit<W>(a.L.block(s, outb[e]) + off, o);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic split-nibble kernel
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(256) generic_kernel(const GenericArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint8_t in_blk[kMaxN + 1];
+  __shared__ uint8_t out_blk[4];
+
+  const uint64_t per_stripe = (uint64_t)a.ctas_per_group * a.n_groups;
+  const uint64_t s = blockIdx.x / per_stripe;
+  const uint32_t rem = (uint32_t)(blockIdx.x % per_stripe);
+  const uint32_t g = rem / a.ctas_per_group, c = rem % a.ctas_per_group;
+  if (s >= a.n_stripes) return;
+  const int pi = a.pat_idx ? a.pat_idx[s] : 0;
+  if (pi < 0) return;
+  const GenericPat &P = a.pats[pi];
+  const int n_in = P.n_in, n_out = P.n_out;
+  if ((int)g * 4 >= n_out) return;
+  const int nr = min(4, n_out - 4 * (int)g);
+
+  constexpr uint32_t TB = (W == 8) ? 128 : 512;  // table bytes per input
+  const uint32_t tb = TB * (uint32_t)n_in;
+  const uint4 *src = reinterpret_cast<const uint4 *>(a.tables + P.table_off + (uint64_t)g * tb);
+  for (uint32_t i = threadIdx.x; i < tb / 16; i += blockDim.x) reinterpret_cast<uint4 *>(smem)[i] = src[i];
+  for (int i = threadIdx.x; i < n_in; i += blockDim.x) in_blk[i] = P.in_blk[i];
+  if ((int)threadIdx.x < nr) out_blk[threadIdx.x] = P.out_blk[4 * g + threadIdx.x];
+  __syncthreads();
+
+  const uint64_t begin = a.col_begin + (uint64_t)c * a.chunk_bytes;
+  const uint64_t end = min(begin + a.chunk_bytes, a.col_end);
+  const uint32_t *T32 = reinterpret_cast<const uint32_t *>(smem);
+  const uint2 *T64 = reinterpret_cast<const uint2 *>(smem);
+
+  for (uint64_t off = begin + (uint64_t)threadIdx.x * 16; off < end; off += (uint64_t)blockDim.x * 16) {
+    if (a.vec_ok && off + 16 <= end) {
+      if (W == 8) {
+        uint32_t acc[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[q] = 0;
+        for (int si = 0; si < n_in; ++si) {
+          const uint4 v = ldg_v4(a.L.block(s, in_blk[si]) + off);
+          const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+          const uint32_t *T = T32 + si * 32;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const uint32_t byte = (wv[q] >> (8 * r)) & 0xFFu;
+              acc[4 * q + r] ^= T[byte & 15u] ^ T[16 + (byte >> 4)];
+            }
+        }
+        for (int r = 0; r < nr; ++r) {
+          uint32_t o[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            o[q] = ((acc[4 * q] >> (8 * r)) & 0xFFu) | (((acc[4 * q + 1] >> (8 * r)) & 0xFFu) << 8) |
+                   (((acc[4 * q + 2] >> (8 * r)) & 0xFFu) << 16) | (((acc[4 * q + 3] >> (8 * r)) & 0xFFu) << 24);
+          stg_v4(a.L.block(s, out_blk[r]) + off, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+      } else {
+        uint2 acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = make_uint2(0, 0);
+        for (int si = 0; si < n_in; ++si) {
+          const uint4 v = ldg_v4(a.L.block(s, in_blk[si]) + off);
+          const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+          const uint2 *T = T64 + si * 64;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t sym = (wv[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+            const uint2 e0 = T[sym & 15u], e1 = T[16 + ((sym >> 4) & 15u)];
+            const uint2 e2 = T[32 + ((sym >> 8) & 15u)], e3 = T[48 + (sym >> 12)];
+            acc[q].x ^= e0.x ^ e1.x ^ e2.x ^ e3.x;
+            acc[q].y ^= e0.y ^ e1.y ^ e2.y ^ e3.y;
+          }
+        }
+        for (int r = 0; r < nr; ++r) {
+          uint32_t o[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t a0 = r < 2 ? acc[2 * q].x : acc[2 * q].y;
+            const uint32_t a1 = r < 2 ? acc[2 * q + 1].x : acc[2 * q + 1].y;
+            o[q] = __byte_perm(a0, a1, (r & 1) ? 0x7632 : 0x5410);
+          }
+          stg_v4(a.L.block(s, out_blk[r]) + off, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+      }
+    } else {
+      // scalar path: ragged tail or unaligned blocks
+      const uint64_t lim = min(off + 16, end);
+      for (uint64_t x = off; x < lim; x += W / 8) {
+        if (W == 8) {
+          uint32_t acc = 0;
+          for (int si = 0; si < n_in; ++si) {
+            const uint32_t byte = a.L.block(s, in_blk[si])[x];
+            acc ^= T32[si * 32 + (byte & 15u)] ^ T32[si * 32 + 16 + (byte >> 4)];
+          }
+          for (int r = 0; r < nr; ++r) a.L.block(s, out_blk[r])[x] = (uint8_t)(acc >> (8 * r));
+        } else {
+          uint2 acc = make_uint2(0, 0);
+          for (int si = 0; si < n_in; ++si) {
+            const uint8_t *p = a.L.block(s, in_blk[si]) + x;
+            const uint32_t sym = (uint32_t)p[0] | ((uint32_t)p[1] << 8);
+            const uint2 *T = T64 + si * 64;
+            const uint2 e0 = T[sym & 15u], e1 = T[16 + ((sym >> 4) & 15u)];
+            const uint2 e2 = T[32 + ((sym >> 8) & 15u)], e3 = T[48 + (sym >> 12)];
+            acc.x ^= e0.x ^ e1.x ^ e2.x ^ e3.x;
+            acc.y ^= e0.y ^ e1.y ^ e2.y ^ e3.y;
+          }
+          for (int r = 0; r < nr; ++r) {
+            const uint32_t v = ((r < 2 ? acc.x : acc.y) >> (16 * (r & 1))) & 0xFFFFu;
+            uint8_t *p = a.L.block(s, out_blk[r]) + x;
+            p[0] = (uint8_t)(v & 0xFF);
+            p[1] = (uint8_t)(v >> 8);
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_generic(int w, const GenericArgs &a, cudaStream_t st) {
+  const uint64_t grid = a.n_stripes * a.n_groups * a.ctas_per_group;
+  if (grid == 0) return cudaSuccess;
+  if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+  count_launch();
+  if (w == 8) {
+    static bool attr8 = (cudaFuncSetAttribute(generic_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              kMaxN * 128) == cudaSuccess);
+    (void)attr8;
+    generic_kernel<8><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
+  } else {
+    static bool attr16 = (cudaFuncSetAttribute(generic_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               kMaxN * 512) == cudaSuccess);
+    (void)attr16;
+    generic_kernel<16><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+bool sliced_available(int k, int m, int w, uint32_t poly) {
+#define RS_AVAIL(K, M, W, P) \
+  if (k == K && m == M && w == W && poly == P) return true;
+  RS_NET_INSTANCES(RS_AVAIL)
+#undef RS_AVAIL
+  return false;
+}
+
+cudaError_t launch_sliced(int k, int m, int w, uint32_t poly, bool decode, const SlicedArgs &a, cudaStream_t st) {
+  const uint64_t grid = a.n_stripes * a.ctas_per_stripe;
+  if (grid == 0) return cudaSuccess;
+  if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+#define RS_LAUNCH(K, M, W, P)                                                  \
+  if (k == K && m == M && w == W && poly == P) {                               \
+    count_launch();                                                            \
+    if (decode) sliced_kernel<K, M, W, P, true><<<(unsigned)grid, 128, 0, st>>>(a);  \
+    else sliced_kernel<K, M, W, P, false><<<(unsigned)grid, 128, 0, st>>>(a);        \
+    return cudaGetLastError();                                                 \
+  }
+  RS_NET_INSTANCES(RS_LAUNCH)
+#undef RS_LAUNCH
+  return cudaErrorNotSupported;
+}
+
+}  // namespace rsb

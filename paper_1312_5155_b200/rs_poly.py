@@ -1,0 +1,203 @@
+"""Thin ctypes binding of include/rs_poly.h (argument marshalling only).
+
+Every computing call goes to librs_poly.so (hand-written sm_100a kernels).  There
+is no CPU fallback: if the library is missing this module raises on import.
+Names follow the C ABI; see the header for argument meaning, layout and errors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "librs_poly.so")
+SYNTH_PATH = os.path.join(_PKG, "librs_synth.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py build` "
+                      "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_vp, _sz, _i32, _u32, _u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64
+_P = ctypes.POINTER
+
+_lib.rs_poly_plan_create.argtypes = [_i32, _i32, _i32, _u32, _P(_vp)]
+_lib.rs_poly_plan_destroy.argtypes = [_vp]
+_lib.rs_poly_plan_destroy.restype = None
+_lib.rs_poly_plan_info.argtypes = [_vp, _vp, _vp]
+_lib.rs_poly_plan_kernel_kind.argtypes = [_vp]
+_lib.rs_poly_encode.argtypes = [_vp, _vp, _vp, _sz, _vp]
+_lib.rs_poly_decode.argtypes = [_vp, _vp, _sz, _vp, _i32, _vp]
+_lib.rs_poly_encode_batch.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp]
+_lib.rs_poly_decode_batch.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _vp]
+_lib.rs_poly_encode_host.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _P(_u64), _P(_u64)]
+_lib.rs_poly_decode_host.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _vp, _P(_u64), _P(_u64)]
+_lib.rs_poly_strerror.argtypes = [_i32]
+_lib.rs_poly_strerror.restype = ctypes.c_char_p
+_lib.rs_poly_abi_version.restype = _i32
+_lib.rs_poly_launch_count.restype = _u64
+
+RS_OK, RS_ERR_INVALID_ARG, RS_ERR_NOT_PRIMITIVE, RS_ERR_GEOMETRY = 0, 1, 2, 3
+RS_ERR_TOO_MANY_ERASURES, RS_ERR_BAD_ERASURE, RS_ERR_CUDA, RS_ERR_NOMEM = 4, 5, 6, 7
+DEFAULT_POLY = {8: 0x11D, 16: 0x1100B}
+
+
+class RSError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        super().__init__(f"{what}: {strerror(status)} (rs_status {status})")
+
+
+def strerror(status: int) -> str:
+    return _lib.rs_poly_strerror(status).decode()
+
+
+def abi_version() -> int:
+    return int(_lib.rs_poly_abi_version())
+
+
+def launch_count() -> int:
+    """Kernels this library has launched since load."""
+    return int(_lib.rs_poly_launch_count())
+
+
+def _check(status: int, what: str) -> None:
+    if status != RS_OK:
+        raise RSError(status, what)
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _ptr(x) -> int:
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    if isinstance(x, np.ndarray):
+        return int(x.ctypes.data)
+    return int(x)
+
+
+def _geometry(stripes, n: int):
+    """(ptr, S, stripe_stride, block_stride, block_bytes) of a [S][n][B] uint8 array/tensor."""
+    shape = tuple(stripes.shape)
+    if len(shape) != 3 or shape[1] != n:
+        raise ValueError(f"expected a [S][{n}][B] uint8 array, got shape {shape}")
+    if hasattr(stripes, "element_size"):
+        if stripes.element_size() != 1:
+            raise ValueError("expected uint8")
+        st = stripes.stride()
+    else:
+        if stripes.dtype != np.uint8:
+            raise ValueError("expected uint8")
+        st = stripes.strides
+    if st[2] != 1:
+        raise ValueError("blocks must be contiguous (last stride 1)")
+    return _ptr(stripes), shape[0], st[0], st[1], shape[2]
+
+
+def _erasure_table(erasures, S: int, m: int) -> np.ndarray:
+    er = np.ascontiguousarray(np.asarray(erasures, dtype=np.int32))
+    if er.shape != (S, m):
+        raise ValueError(f"erasures must be int32 [{S}][{m}] (-1 padded)")
+    return er
+
+
+class Plan:
+    """An RS(k, m) code over GF(2^w) with alpha = 2 (rs_poly_plan_create)."""
+
+    def __init__(self, k: int, m: int, w: int = 8, prim_poly: int | None = None):
+        self.k, self.m, self.w = k, m, w
+        self.n = k + m
+        self.prim_poly = DEFAULT_POLY.get(w, 0) if prim_poly is None else prim_poly
+        h = _vp()
+        _check(_lib.rs_poly_plan_create(k, m, w, self.prim_poly, ctypes.byref(h)), "rs_poly_plan_create")
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.rs_poly_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def kernel_kind(self) -> str:
+        return "bitsliced" if _lib.rs_poly_plan_kernel_kind(self._h) == 1 else "generic"
+
+    def info(self):
+        """(g low->high, parity map [m][k]) -- host-only."""
+        g = np.zeros(self.m + 1, dtype=np.uint32)
+        P = np.zeros((self.m, self.k), dtype=np.uint32)
+        _check(_lib.rs_poly_plan_info(self._h, g.ctypes.data, P.ctypes.data), "rs_poly_plan_info")
+        return g, P
+
+    # ---- single stripe -------------------------------------------------------
+    def encode(self, data, parity, block_bytes: int, stream=None) -> None:
+        d = (ctypes.c_void_p * self.k)(*[_ptr(x) for x in data])
+        p = (ctypes.c_void_p * self.m)(*[_ptr(x) for x in parity])
+        _check(_lib.rs_poly_encode(self._h, d, p, block_bytes, _stream(stream)), "rs_poly_encode")
+
+    def decode(self, blocks, block_bytes: int, erasures, stream=None) -> None:
+        b = (ctypes.c_void_p * self.n)(*[_ptr(x) for x in blocks])
+        er = list(erasures)
+        e = (ctypes.c_int * max(1, len(er)))(*er)
+        _check(_lib.rs_poly_decode(self._h, b, block_bytes, e, len(er), _stream(stream)), "rs_poly_decode")
+
+    # ---- batched (device memory) ----------------------------------------------
+    def encode_batch(self, stripes, stream=None) -> None:
+        ptr, S, ss, bs, B = _geometry(stripes, self.n)
+        _check(_lib.rs_poly_encode_batch(self._h, ptr, S, ss, bs, B, _stream(stream)), "rs_poly_encode_batch")
+
+    def decode_batch(self, stripes, erasures, stream=None) -> None:
+        ptr, S, ss, bs, B = _geometry(stripes, self.n)
+        er = _erasure_table(erasures, S, self.m)
+        _check(_lib.rs_poly_decode_batch(self._h, ptr, S, ss, bs, B, er.ctypes.data, _stream(stream)),
+               "rs_poly_decode_batch")
+
+    # ---- end to end from host memory --------------------------------------------
+    def encode_host(self, host_stripes, stream=None):
+        ptr, S, ss, bs, B = _geometry(host_stripes, self.n)
+        h2d, d2h = _u64(), _u64()
+        _check(_lib.rs_poly_encode_host(self._h, ptr, S, ss, bs, B, _stream(stream), ctypes.byref(h2d),
+                                        ctypes.byref(d2h)), "rs_poly_encode_host")
+        return int(h2d.value), int(d2h.value)
+
+    def decode_host(self, host_stripes, erasures, stream=None):
+        ptr, S, ss, bs, B = _geometry(host_stripes, self.n)
+        er = _erasure_table(erasures, S, self.m)
+        h2d, d2h = _u64(), _u64()
+        _check(_lib.rs_poly_decode_host(self._h, ptr, S, ss, bs, B, er.ctypes.data, _stream(stream),
+                                        ctypes.byref(h2d), ctypes.byref(d2h)), "rs_poly_decode_host")
+        return int(h2d.value), int(d2h.value)
+
+
+# ---- on-device input generator (librs_synth.so; not the method) ---------------
+_synth = None
+
+
+def synth_fill(stripes, k: int, seed: int, stripe0: int = 0, stream=None) -> None:
+    """Fill data blocks 0..k-1 of a [S][n][B] device array with the synth/ recipe."""
+    global _synth
+    if _synth is None:
+        _synth = ctypes.CDLL(SYNTH_PATH)
+        _synth.rs_synth_fill.argtypes = [_vp, _sz, _sz, _sz, _sz, _i32, _u32, _u32, _vp]
+    shape = tuple(stripes.shape)
+    ptr, S, ss, bs, B = _ptr(stripes), shape[0], stripes.stride()[0], stripes.stride()[1], shape[2]
+    rc = _synth.rs_synth_fill(ptr, S, ss, bs, B, k, seed, stripe0, _stream(stream))
+    if rc != 0:
+        raise RuntimeError(f"rs_synth_fill failed ({rc})")
