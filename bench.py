@@ -1,0 +1,392 @@
+#!/usr/bin/env python3
+"""bench.py -- RS-poly encode + decode throughput on B200 (BASELINE.json metric).
+
+One STEP = one pass of the whole hot path over the batch resident in HBM:
+rs_poly_encode_batch (parity = d(x) x^m mod g(x)) followed by
+rs_poly_decode_batch with a per-stripe erasure pattern.  Each pass
+counts the batch's user data S*k*B once, so value = 2*S*k*B*N / max-rank time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5|C3|C4]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+  python bench.py --impl reference ...   # the CPU oracle, timed on this host's cores
+
+Default workload: BASELINE.json configs[4] (C5): RS(10,4) over GF(2^8)/0x11D,
+51 stripes x 10 x 16 MiB of synthetic data per GPU (seed = rank), 4 random erasures
+per stripe -- the config the metric is quoted on ("per GPU and at 8xB200").
+Stripes shard across ranks with no data exchange (weak scaling); NCCL only carries
+the barrier and the max-over-ranks time / summed mismatch counts.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (seeded input generator shared by both sides)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+METRIC = "RS poly encode/decode GB/s of data per GPU and at 8×B200; % of HBM roofline"
+
+WORKLOADS = {
+    "C5": "RS(10,4) GF(2^8)/0x11D, 51 stripes x 10 x 16 MiB per GPU (seed=rank), encode + 4-random-erasure decode",
+    "C3": "RS(10,4) GF(2^8)/0x11D, 512 stripes x 10 x 4 MiB per GPU, encode + decode with 4 erasures "
+          "(even stripes data-only)",
+    "C4": "RS(12,4) GF(2^16)/0x1100B LE uint16, 256 stripes x 12 x 8 MiB per GPU, encode + 4-erasure decode",
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None, help="end-to-end steps (default: min(steps, 5))")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample duration")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def workload(cfg: str, rank: int):
+    c = dict(synth.CONFIGS[cfg])
+    c["seed"] = rank  # C5: seed = rank (BASELINE.json); other configs: seed 0 on rank 0
+    c["n"] = c["k"] + c["m"]
+    c["name"] = cfg
+    return c
+
+
+# --------------------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference)
+# --------------------------------------------------------------------------------------
+def oracle_sample(c, n_stripes: int, block_prefix: int):
+    """Host copy of the first `block_prefix` bytes of every block of stripes 0..n_stripes-1
+    (columns are independent codewords, so a column prefix is a valid sub-workload)."""
+    st = synth.stripes_array(c["seed"], range(n_stripes), c["k"], c["m"], block_prefix)
+    er = synth.erasure_table(c["name"], c["seed"], n_stripes)
+    return st, er
+
+
+def oracle_pass(oracle, st, er, c, threads):
+    oracle.encode_bulk(st, c["k"], c["m"], c["w"], c["poly"], threads=threads)
+    oracle.decode_bulk(st, er, c["k"], c["m"], c["w"], c["poly"], threads=threads)
+
+
+def cpu_baseline(c, seconds: float):
+    import oracle
+    cores = os.cpu_count() or 1
+    threads = max(1, min(cores, c["stripes"]))
+    prefix = min(c["block_bytes"], 2 << 20)
+    st, er = oracle_sample(c, threads, prefix)
+    oracle_pass(oracle, st, er, c, threads)  # warm
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        oracle_pass(oracle, st, er, c, threads)
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    user = threads * c["k"] * prefix
+    return {"value": round(2 * user * passes / el / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"{threads} stripes x {c['k']} data blocks x first {prefix} B of each block "
+                      f"({user / 2**20:.0f} MiB user data), encode + decode with the config's erasure patterns, "
+                      f"{passes} passes in {el:.1f} s, {threads} threads (one stripe each) of {cores} host cores"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    c = workload(args.config, 0)
+    cores = os.cpu_count() or 1
+    threads = max(1, min(cores, c["stripes"]))
+    prefix = min(c["block_bytes"], 2 << 20)
+    st, er = oracle_sample(c, threads, prefix)
+    for _ in range(args.warmup):
+        oracle_pass(oracle, st, er, c, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_pass(oracle, st, er, c, threads)
+    el = time.perf_counter() - t0
+    user = threads * c["k"] * prefix
+    value = 2 * user * args.steps / el / 1e9
+    sample = (f"per step: {threads} stripes x {c['k']} data blocks x first {prefix} B of each block of the "
+              f"{args.config} workload, encode + decode; {threads} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8" if c["w"] == 8 else "u16", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {WORKLOADS[args.config]}", "k": c["k"], "m": c["m"], "w": c["w"],
+                   "prim_poly": hex(c["poly"]), "block_bytes": c["block_bytes"], "stripes_per_gpu": c["stripes"],
+                   "parallelism": f"dp{args.gpus}"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# --------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index: int, period: float = 0.005):
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------------------
+# GPU leg
+# --------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1312_5155_b200 as rsp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def allreduce(x: float, op):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    c = workload(args.config, rank)
+    k, m, n, w, B, S = c["k"], c["m"], c["n"], c["w"], c["block_bytes"], c["stripes"]
+    plan = rsp.Plan(k, m, w, c["poly"])
+    stream = torch.cuda.current_stream()
+    stripes = torch.empty((S, n, B), dtype=torch.uint8, device=dev)
+    rsp.synth_fill(stripes, k, seed=c["seed"], stripe0=0)
+    er = synth.erasure_table(args.config, c["seed"], S)
+    er_t = [torch.from_numpy(er[s][er[s] >= 0].astype(np.int64)).to(dev) for s in range(S)]
+
+    # ---- correctness before any number: encode vs the oracle on sampled columns,
+    # and decode restores every byte of every stripe (exact compare on device) ----
+    plan.encode_batch(stripes)
+    torch.cuda.synchronize()
+    mismatches = verify_encode_sampled(stripes, c)
+    golden = stripes.clone()
+    for s in range(S):
+        stripes[s].index_fill_(0, er_t[s], 0xEE)
+    plan.decode_batch(stripes, er)
+    torch.cuda.synchronize()
+    mismatches += 0 if torch.equal(stripes, golden) else 1
+    del golden
+    torch.cuda.empty_cache()
+
+    # ---- warm-up ----
+    for _ in range(args.warmup):
+        plan.encode_batch(stripes)
+        plan.decode_batch(stripes, er)
+    barrier()
+
+    # ---- timed region: K steps, per-call CUDA events on the launching stream ----
+    K = args.steps
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * K + 1)]
+    clk = ClockSampler(local).start()
+    launches0 = rsp.launch_count()
+    barrier()
+    ev[0].record(stream)
+    for i in range(K):
+        plan.encode_batch(stripes)
+        ev[2 * i + 1].record(stream)
+        plan.decode_batch(stripes, er)
+        ev[2 * i + 2].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    launches = rsp.launch_count() - launches0
+    enc_ms = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(K)]
+    dec_ms = [ev[2 * i + 1].elapsed_time(ev[2 * i + 2]) for i in range(K)]
+    total_ms = ev[0].elapsed_time(ev[2 * K])
+    total_ms = allreduce(total_ms, dist.ReduceOp.MAX if world > 1 else None)
+    enc_avg, dec_avg = statistics.mean(enc_ms), statistics.mean(dec_ms)
+
+    # post-run check: the timed passes reproduced the verified batch
+    plan.encode_batch(stripes)
+    torch.cuda.synchronize()
+    mismatches += verify_encode_sampled(stripes, c)
+    mismatches = int(allreduce(float(mismatches), dist.ReduceOp.SUM if world > 1 else None))
+
+    user_bytes = S * k * B                      # per GPU per pass
+    moved = S * (k + m) * B                     # HBM bytes per pass (read once or written once)
+    value = 2 * user_bytes * world / (total_ms / K / 1e3) / 1e9
+    peak, peak_src = hbm_peak()
+    dom_ms, dom_name = (dec_avg, "decode") if dec_avg >= enc_avg else (enc_avg, "encode")
+    achieved = moved / (dom_ms / 1e3) / 1e9
+
+    # ---- end to end through the public API from pinned host memory ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, plan, stripes, er, c, world, allreduce, barrier, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(c, args.cpu_seconds)
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / K, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8" if w == 8 else "u16", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {WORKLOADS[args.config]}", "k": k, "m": m, "w": w,
+                   "prim_poly": hex(c["poly"]), "block_bytes": B, "stripes_per_gpu": S,
+                   "bytes_per_gpu": S * n * B, "parallelism": f"dp{world}",
+                   "kernels": plan.kernel_kind,
+                   "l2": f"inputs {S * n * B / 2**30:.1f} GiB per GPU >> 126 MB L2: no flush needed"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": f"{dom_name} (sliced_kernel), {moved} algorithmic bytes per launch = "
+                               f"S*(k+m)*B, avg {dom_ms:.4f} ms", "peak_source": peak_src},
+        "encode": {"gbs_user": round(user_bytes / (enc_avg / 1e3) / 1e9, 2), "ms": round(enc_avg, 4),
+                   "hbm_frac": round(moved / (enc_avg / 1e3) / 1e9 / peak, 4)},
+        "decode": {"gbs_user": round(user_bytes / (dec_avg / 1e3) / 1e9, 2), "ms": round(dec_avg, 4),
+                   "hbm_frac": round(moved / (dec_avg / 1e3) / 1e9 / peak, 4)},
+        "verified": {"mismatches": mismatches,
+                     "how": "encode vs CPU oracle on sampled columns of 3 stripes (before and after timing); "
+                            "decode restores all S*n*B bytes (exact device compare)"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0 if mismatches == 0 else 1
+
+
+def verify_encode_sampled(stripes, c) -> int:
+    """Oracle re-encode of sampled columns (first/last 64 KiB of every block) of stripes 0, S/2, S-1."""
+    import oracle
+    k, m, n, w, B, S = c["k"], c["m"], c["n"], c["w"], c["block_bytes"], c["stripes"]
+    span = min(B // 2, 64 << 10) // (w // 8) * (w // 8)
+    bad = 0
+    for s in sorted({0, S // 2, S - 1}):
+        host = synth.stripes_array(c["seed"], [s], k, m, B)
+        cols = np.concatenate([host[:, :, :span], host[:, :, B - span:]], axis=2).copy()
+        oracle.encode_bulk(cols, k, m, w, c["poly"], threads=2)
+        got = stripes[s].cpu().numpy()
+        got = np.concatenate([got[None, :, :span], got[None, :, B - span:]], axis=2)
+        bad += int(not np.array_equal(got, cols))
+    return bad
+
+
+def run_e2e(args, plan, stripes, er, c, world, allreduce, barrier, dist):
+    import torch
+    K = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 5)
+    K = max(1, K)
+    S, k, B = c["stripes"], c["k"], c["block_bytes"]
+    host = torch.empty(tuple(stripes.shape), dtype=torch.uint8, pin_memory=True)
+    host.copy_(stripes)
+    plan.encode_host(host)  # warm
+    plan.decode_host(host, er)
+    barrier()
+    t0 = time.perf_counter()
+    h2d = d2h = 0
+    for _ in range(K):
+        a, b = plan.encode_host(host)
+        c2, d = plan.decode_host(host, er)
+        h2d += a + c2
+        d2h += b + d
+    barrier()
+    el = allreduce(time.perf_counter() - t0, dist.ReduceOp.MAX if world > 1 else None)
+    ok = torch.equal(host, stripes.cpu())
+    value = 2 * S * k * B * world / (el / K) / 1e9
+    return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K,
+            "steps": K, "ms_per_step": round(el / K * 1e3, 3), "verified": bool(ok),
+            "how": "rs_poly_encode_host + rs_poly_decode_host on pinned host stripes; host->device inputs, "
+                   "device->host outputs inside the timed region (wall clock, max over ranks)"}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

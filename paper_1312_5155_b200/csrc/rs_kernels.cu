@@ -59,22 +59,34 @@ __device__ __forceinline__ void stg_v8(void *p, const uint32_t *r) {
 // bit-plane transposes (delta swaps; each is an involution, so the same
 // routine goes bytes -> planes and planes -> bytes)
 // ---------------------------------------------------------------------------
-// Left shift on the FMA pipe (IMAD.SHL), right shift on the ALU pipe (SHF):
-// the ALU pipe (64 lanes/clk/SM on B200) is the scarce one.
+// Shifts run on the FMA pipe (IMAD.SHL / IMAD.HI): on B200 the ALU pipe
+// (LOP3/SHF/PRMT, 64 lanes/clk/SM) is the scarce one, the FMA pipe is mostly idle
+// (profiles/r01_microbench_pipes.log: IMAD 128/clk/SM, mul.hi 32/clk/SM).
 template <int S>
 __device__ __forceinline__ uint32_t shl_fma(uint32_t v) {
   uint32_t r;
   asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(v), "n"(1u << S));
   return r;
 }
+template <int S>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t v) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(v), "n"(1u << (32 - S)));
+  return r;
+}
+// MASK ? a : b in ONE LOP3 (ptxas otherwise splits a&M | b&~M into two).
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "n"(MASK));
+  return r;
+}
 
 // Swap in-word bit S-position (mask ~M) of a with word-index bit of c.
 template <int S, uint32_t MASK>
 __device__ __forceinline__ void delta_swap(uint32_t &a, uint32_t &c) {
-  const uint32_t cs = shl_fma<S>(c);
-  const uint32_t as = a >> S;
-  const uint32_t na = (a & MASK) | (cs & ~MASK);
-  const uint32_t nc = (as & MASK) | (c & ~MASK);
+  const uint32_t na = bitsel<MASK>(a, shl_fma<S>(c));
+  const uint32_t nc = bitsel<MASK>(shr_fma<S>(a), c);
   a = na;
   c = nc;
 }
@@ -226,10 +238,10 @@ __global__ void __launch_bounds__(128) sliced_kernel(const SlicedArgs a) {
         for (int q = 0; q < 8; ++q) {
           const uint32_t v = y[i * W + q];
           const uint32_t lo = shl_fma<2>(v) & 0x3C3C3C3Cu;  // low nibbles * 4 (byte offsets)
-          const uint32_t hi = (v >> 2) & 0x3C3C3C3Cu;       // high nibbles * 4
+          const uint32_t hi = shr_fma<2>(v) & 0x3C3C3C3Cu;  // high nibbles * 4
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            const uint32_t il = (lo >> (8 * r)) & 0xFFu, ih = (hi >> (8 * r)) & 0xFFu;
+            const uint32_t il = __byte_perm(lo, 0, 0x4440 + r), ih = __byte_perm(hi, 0, 0x4440 + r);
             acc[4 * q + r] ^= *reinterpret_cast<const uint32_t *>(Tl + il) ^
                               *reinterpret_cast<const uint32_t *>(Th + ih);
           }
@@ -263,11 +275,11 @@ __global__ void __launch_bounds__(128) sliced_kernel(const SlicedArgs a) {
         for (int q = 0; q < 16; ++q) {
           const uint32_t v = y[i * W + q];
           const uint32_t lo = shl_fma<3>(v) & 0x78787878u;  // nibbles 0,2 of both symbols * 8
-          const uint32_t hi = (v >> 1) & 0x78787878u;       // nibbles 1,3 * 8
+          const uint32_t hi = shr_fma<1>(v) & 0x78787878u;  // nibbles 1,3 * 8
 #pragma unroll
           for (int r = 0; r < 2; ++r) {  // symbol r of the word = column 2q+r
-            const uint32_t n0 = (lo >> (16 * r)) & 0xFFu, n2 = (lo >> (16 * r + 8)) & 0xFFu;
-            const uint32_t n1 = (hi >> (16 * r)) & 0xFFu, n3 = (hi >> (16 * r + 8)) & 0xFFu;
+            const uint32_t n0 = __byte_perm(lo, 0, 0x4440 + 2 * r), n2 = __byte_perm(lo, 0, 0x4441 + 2 * r);
+            const uint32_t n1 = __byte_perm(hi, 0, 0x4440 + 2 * r), n3 = __byte_perm(hi, 0, 0x4441 + 2 * r);
             const uint2 e0 = *reinterpret_cast<const uint2 *>(T0 + 0 * 128 + n0);
             const uint2 e1 = *reinterpret_cast<const uint2 *>(T0 + 1 * 128 + n1);
             const uint2 e2 = *reinterpret_cast<const uint2 *>(T0 + 2 * 128 + n2);
