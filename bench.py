@@ -67,6 +67,22 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def allreduce(x: float, op: str, world: int, device) -> float:
+    """Max/sum of a scalar over ranks (NCCL on the GPU box; gloo in tests/test_dist_gloo.py)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "sum": dist.ReduceOp.SUM}[op])
+    return float(t.item())
+
+
+def step_throughput(user_bytes_per_gpu: int, passes: int, world: int, max_step_ms: float) -> float:
+    """Whole-job GB/s of user data: every rank processes its own stripes (weak scaling)."""
+    return passes * user_bytes_per_gpu * world / (max_step_ms / 1e3) / 1e9
+
+
 def workload(cfg: str, rank: int):
     c = dict(synth.CONFIGS[cfg])
     c["seed"] = rank  # C5: seed = rank (BASELINE.json); other configs: seed 0 on rank 0
@@ -219,13 +235,6 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    def allreduce(x: float, op):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=op)
-        return float(t.item())
-
     def barrier():
         if world > 1:
             dist.barrier()
@@ -279,18 +288,18 @@ def run_ours(args):
     enc_ms = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(K)]
     dec_ms = [ev[2 * i + 1].elapsed_time(ev[2 * i + 2]) for i in range(K)]
     total_ms = ev[0].elapsed_time(ev[2 * K])
-    total_ms = allreduce(total_ms, dist.ReduceOp.MAX if world > 1 else None)
+    total_ms = allreduce(total_ms, "max", world, dev)
     enc_avg, dec_avg = statistics.mean(enc_ms), statistics.mean(dec_ms)
 
     # post-run check: the timed passes reproduced the verified batch
     plan.encode_batch(stripes)
     torch.cuda.synchronize()
     mismatches += verify_encode_sampled(stripes, c)
-    mismatches = int(allreduce(float(mismatches), dist.ReduceOp.SUM if world > 1 else None))
+    mismatches = int(allreduce(float(mismatches), "sum", world, dev))
 
     user_bytes = S * k * B                      # per GPU per pass
     moved = S * (k + m) * B                     # HBM bytes per pass (read once or written once)
-    value = 2 * user_bytes * world / (total_ms / K / 1e3) / 1e9
+    value = step_throughput(user_bytes, 2, world, total_ms / K)
     peak, peak_src = hbm_peak()
     dom_ms, dom_name = (dec_avg, "decode") if dec_avg >= enc_avg else (enc_avg, "encode")
     achieved = moved / (dom_ms / 1e3) / 1e9
@@ -298,7 +307,7 @@ def run_ours(args):
     # ---- end to end through the public API from pinned host memory ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, plan, stripes, er, c, world, allreduce, barrier, dist)
+        e2e = run_e2e(args, plan, stripes, er, c, world, dev, barrier)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -354,7 +363,7 @@ def verify_encode_sampled(stripes, c) -> int:
     return bad
 
 
-def run_e2e(args, plan, stripes, er, c, world, allreduce, barrier, dist):
+def run_e2e(args, plan, stripes, er, c, world, dev, barrier):
     import torch
     K = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 5)
     K = max(1, K)
@@ -372,9 +381,9 @@ def run_e2e(args, plan, stripes, er, c, world, allreduce, barrier, dist):
         h2d += a + c2
         d2h += b + d
     barrier()
-    el = allreduce(time.perf_counter() - t0, dist.ReduceOp.MAX if world > 1 else None)
+    el = allreduce(time.perf_counter() - t0, "max", world, dev)
     ok = torch.equal(host, stripes.cpu())
-    value = 2 * S * k * B * world / (el / K) / 1e9
+    value = step_throughput(S * k * B, 2, world, el / K * 1e3)
     return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K,
             "steps": K, "ms_per_step": round(el / K * 1e3, 3), "verified": bool(ok),
             "how": "rs_poly_encode_host + rs_poly_decode_host on pinned host stripes; host->device inputs, "

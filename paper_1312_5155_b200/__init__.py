@@ -6,6 +6,8 @@
     plan.decode_batch(stripes, erasures)   # erasures: int32 [S][4], -1 padded
 """
 from .rs_poly import (DEFAULT_POLY, LIB_PATH, SYNTH_PATH, Plan, RSError, abi_version, launch_count,  # noqa: F401
+                      RS_OK, RS_ERR_INVALID_ARG, RS_ERR_NOT_PRIMITIVE, RS_ERR_GEOMETRY, RS_ERR_TOO_MANY_ERASURES,
+                      RS_ERR_BAD_ERASURE, RS_ERR_CUDA, RS_ERR_NOMEM,
                       strerror, synth_fill)
 
 __all__ = ["Plan", "RSError", "synth_fill", "launch_count", "abi_version", "strerror", "DEFAULT_POLY"]

@@ -1,0 +1,80 @@
+"""The N>1 harness path of bench.py on CPU: world_size 2 over gloo.
+
+The data path does not communicate (stripes shard by rank); the
+process group only carries the barrier, the max-over-ranks time and the summed
+mismatch count.  This checks those reductions, the per-rank sharding of the
+synthetic workload, and that the reference arm runs on rank 0 only.
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    import bench
+    import synth
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = bench.allreduce(10.0 + rank, "max", world, "cpu")
+    mism = bench.allreduce(float(rank), "sum", world, "cpu")
+    c = bench.workload("C5", rank)
+    er = synth.erasure_table("C5", c["seed"], c["stripes"])
+    first = synth.data_block(c["seed"], 0, 0, 64)
+    dist.barrier()
+    out[rank] = dict(t=t, mism=mism, seed=c["seed"], er=er.tolist(), first=first.tolist())
+    dist.destroy_process_group()
+
+
+def test_two_rank_reductions_and_sharding():
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    r0, r1 = out[0], out[1]
+    assert r0["t"] == r1["t"] == 11.0          # max over ranks
+    assert r0["mism"] == r1["mism"] == 1.0     # sum over ranks
+    assert (r0["seed"], r1["seed"]) == (0, 1)  # C5: seed = rank
+    assert r0["er"] != r1["er"] and r0["first"] != r1["first"]  # disjoint synthetic shards
+
+
+def test_step_throughput_weak_scaling():
+    import bench
+    one = bench.step_throughput(10 << 20, 2, 1, 5.0)
+    eight = bench.step_throughput(10 << 20, 2, 8, 5.0)
+    assert abs(eight - 8 * one) < 1e-9
+    assert abs(one - 2 * (10 << 20) / 5e-3 / 1e9) < 1e-9
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    """--impl reference under the launcher: rank 0 prints one JSON line, rank 1 exits 0 silently."""
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--config", "C5"]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert np.isfinite(d["ms_per_step"])
