@@ -169,8 +169,15 @@ __device__ __forceinline__ void net_groups(uint8_t *const *blk, uint64_t off, ui
 // ---------------------------------------------------------------------------
 // bit-sliced kernel
 // ---------------------------------------------------------------------------
+// Resident CTAs per SM (x 128 threads): the kernels hide HBM latency with warps, so
+// occupancy matters more than registers.  Measured on B200 (profiles/r01b_occupancy_sweep.log):
+// w8 at 4 CTAs/SM (<=128 regs, a few spilled bytes) reaches the copy roofline on RS(10,4)
+// encode; w16 spills at 4 and runs best at 3.
+template <int W>
+constexpr int sliced_min_blocks() { return W == 8 ? 4 : 3; }
+
 template <int K, int M, int W, uint32_t POLY, bool DECODE>
-__global__ void __launch_bounds__(128) sliced_kernel(const SlicedArgs a) {
+__global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(const SlicedArgs a) {
   constexpr int UB = 32 * W / 8;                    // bytes per unit per block
   constexpr int TAB_WORDS = M * (W / 4) * 16 * (W / 8);  // W-step tables, 32-bit words
   __shared__ __align__(16) uint32_t wtab[DECODE ? TAB_WORDS : 1];

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "librs_poly.so")
+LIB_PATH = os.environ.get("RS_POLY_LIB") or os.path.join(_PKG, "librs_poly.so")
 SYNTH_PATH = os.path.join(_PKG, "librs_synth.so")
 
 if not os.path.exists(LIB_PATH):
