@@ -128,6 +128,49 @@ rs_status rs_poly_decode_host(const rs_poly_plan *plan, void *host_stripes, size
                               const int32_t *erasures, void *stream, uint64_t *h2d_bytes,
                               uint64_t *d2h_bytes);
 
+/* ---- run-time specialised kernels (JIT) ----------------------------------------
+ * For every erasure pattern E the decode map survivors -> erased symbols is a fixed
+ * GF(2)-linear map (R_E = V_E^{-1} A_E, the paper's Step 1 + Step 2 with Opt1/Opt3
+ * precomputed once per pattern).  With JIT on, the plan compiles (NVRTC,
+ * sm_100a) a bit-sliced XOR-network kernel for each pattern it meets, exactly like
+ * the compiled encoder, and uses it once ready; until then (or if NVRTC is absent)
+ * the table-driven kernels serve the pattern.  Results are identical either way.
+ * Codes without a compiled encoder network get a JIT encoder the same way.
+ *   RS_JIT_OFF        never compile (table-driven kernels only)
+ *   RS_JIT_BACKGROUND compile on a worker pool, never block a call (default)
+ *   RS_JIT_SYNC       compile inside the first call that meets a pattern
+ * rs_poly_plan_set_jit is a configuration call: make it before sharing the plan. */
+#define RS_JIT_OFF 0
+#define RS_JIT_BACKGROUND 1
+#define RS_JIT_SYNC 2
+rs_status rs_poly_plan_set_jit(rs_poly_plan *plan, int mode);
+
+/* Precompute (Opt1/Opt3) the decode constants of every pattern listed in
+ * `erasures` (HOST int32 [n_rows][m], -1 padded, as in rs_poly_decode_batch) and,
+ * unless JIT is off, compile their kernels, blocking until they are ready.  Also
+ * compiles the JIT encoder for codes without a compiled one.  Host + NVRTC only; no
+ * kernel runs.  Returns RS_OK even if a compile fails (those patterns keep the
+ * table-driven kernels; see rs_poly_plan_stats). */
+rs_status rs_poly_prepare(const rs_poly_plan *plan, const int32_t *erasures, size_t n_rows);
+
+typedef struct {
+  uint64_t patterns;       /* decode patterns in the cache                        */
+  uint64_t jit_ready;      /* JIT kernels compiled and loaded                     */
+  uint64_t jit_pending;    /* JIT compiles in flight                              */
+  uint64_t jit_failed;     /* JIT compiles that failed (NVRTC missing or error)   */
+  uint64_t jit_launches;   /* kernel launches that used a JIT kernel              */
+  uint64_t table_launches; /* decode body launches that used the table kernels    */
+  int jit_available;       /* 1 if NVRTC could be loaded                          */
+  int jit_mode;
+} rs_poly_stats;
+rs_status rs_poly_plan_stats(const rs_poly_plan *plan, rs_poly_stats *out);
+
+/* Introspection: the CUDA source the JIT generates for erasure list `erasures`
+ * (n_erasures >= 1), or for the encoder when n_erasures == 0.  Copies at most cap
+ * bytes (NUL-terminated when cap > 0) into buf and returns the full length, or 0 if
+ * the arguments are invalid or the pattern is not JIT-eligible.  Host only. */
+size_t rs_poly_jit_source(const rs_poly_plan *plan, const int *erasures, int n_erasures, char *buf, size_t cap);
+
 /* ---- misc ----------------------------------------------------------------- */
 const char *rs_poly_strerror(rs_status status);
 int rs_poly_abi_version(void);

@@ -38,6 +38,15 @@ def _run(cmd: list[str]) -> None:
     subprocess.check_call(cmd)
 
 
+def _embed(src: str, dst: str, name: str) -> None:
+    """Write `src` as a C++ raw string literal (the JIT prepends it to generated kernels)."""
+    text = open(src).read()
+    body = f'static const char {name}[] = R"RSJIT({text})RSJIT";\n'
+    if not os.path.exists(dst) or open(dst).read() != body:
+        with open(dst, "w") as f:
+            f.write(body)
+
+
 def build(verbose_ptxas: bool = False) -> list[str]:
     sys.path.insert(0, CSRC)
     try:
@@ -45,13 +54,15 @@ def build(verbose_ptxas: bool = False) -> list[str]:
         gen_networks.generate()
     finally:
         sys.path.pop(0)
-    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp")) + \
+    _embed(os.path.join(CSRC, "bitslice_device.cuh"), os.path.join(CSRC, "bitslice_device_src.inc"),
+           "kBitsliceDeviceSrc")
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.inc")) + glob.glob(os.path.join(CSRC, "*.hpp")) + \
         glob.glob(os.path.join(INCLUDE, "*.h"))
-    poly_src = [os.path.join(CSRC, "rs_kernels.cu"), os.path.join(CSRC, "plan.cpp")]
+    poly_src = [os.path.join(CSRC, "rs_kernels.cu"), os.path.join(CSRC, "plan.cpp"), os.path.join(CSRC, "jit.cpp")]
     extra = ["-Xptxas", "-v"] if verbose_ptxas else []
     if _stale(POLY_LIB, poly_src + headers + [__file__]):
         tmp = POLY_LIB + ".tmp%d" % os.getpid()
-        _run([NVCC] + FLAGS + extra + ["-shared", "-o", tmp] + poly_src)
+        _run([NVCC] + FLAGS + extra + ["-shared", "-o", tmp] + poly_src + ["-ldl"])
         os.replace(tmp, POLY_LIB)
     synth_src = [os.path.join(CSRC, "synth.cu")]
     if _stale(SYNTH_LIB, synth_src + [os.path.join(INCLUDE, "rs_synth.h"), __file__]):

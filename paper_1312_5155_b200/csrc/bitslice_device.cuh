@@ -1,0 +1,126 @@
+// bitslice_device.cuh -- device helpers shared by the compiled kernels (rs_kernels.cu)
+// and the per-pattern kernels generated at run time (jit.cpp, NVRTC).  Self-contained:
+// NVRTC compiles it without any system header.
+#pragma once
+#ifdef __CUDACC_RTC__
+typedef unsigned char uint8_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+#else
+#include <cstdint>
+#endif
+
+namespace rsb {
+
+// ---------------------------------------------------------------------------
+// memory helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ldg_v4(const void *p) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg_v4(void *p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void ldg_v8(const void *p, uint32_t *r) {
+  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void stg_v8(void *p, const uint32_t *r) {
+  asm volatile("st.global.L1::no_allocate.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+                  "r"(r[7])
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// bit-plane transposes (delta swaps; each is an involution, so the same
+// routine goes bytes -> planes and planes -> bytes)
+// ---------------------------------------------------------------------------
+// Shifts run on the FMA pipe (IMAD.SHL / IMAD.HI): on B200 the ALU pipe
+// (LOP3/SHF/PRMT, 64 lanes/clk/SM) is the scarce one, the FMA pipe is mostly idle
+// (profiles/r01_microbench_pipes.log: IMAD 128/clk/SM, mul.hi 32/clk/SM).
+template <int S>
+__device__ __forceinline__ uint32_t shl_fma(uint32_t v) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(v), "n"(1u << S));
+  return r;
+}
+template <int S>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t v) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(v), "n"(1u << (32 - S)));
+  return r;
+}
+// MASK ? a : b in ONE LOP3 (ptxas otherwise splits a&M | b&~M into two).
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "n"(MASK));
+  return r;
+}
+
+// Swap in-word bit S-position (mask ~M) of a with word-index bit of c.
+template <int S, uint32_t MASK>
+__device__ __forceinline__ void delta_swap(uint32_t &a, uint32_t &c) {
+  const uint32_t na = bitsel<MASK>(a, shl_fma<S>(c));
+  const uint32_t nc = bitsel<MASK>(shr_fma<S>(a), c);
+  a = na;
+  c = nc;
+}
+
+// 8 words (32 columns of bytes; word i = columns 4i..4i+3) <-> 8 planes
+// (plane b = bit b of the 32 columns; column 4i+r at plane bit 8r+i).
+__device__ __forceinline__ void transpose8(uint32_t *x) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) delta_swap<4, 0x0F0F0F0Fu>(x[i], x[i + 4]);
+#pragma unroll
+  for (int i = 0; i < 8; i += 4) {
+    delta_swap<2, 0x33333333u>(x[i], x[i + 2]);
+    delta_swap<2, 0x33333333u>(x[i + 1], x[i + 3]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) delta_swap<1, 0x55555555u>(x[i], x[i + 1]);
+}
+
+// 16 words (32 columns of LE uint16; word i = columns 2i, 2i+1) <-> 16 planes
+// (plane b = bit b; column 2i+r at plane bit 16r+i).  The byte stage uses PRMT.
+__device__ __forceinline__ void transpose16(uint32_t *x) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t a = x[i], c = x[i + 8];
+    x[i] = __byte_perm(a, c, 0x6240);
+    x[i + 8] = __byte_perm(a, c, 0x7351);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if ((i & 4) == 0) delta_swap<4, 0x0F0F0F0Fu>(x[i], x[i + 4]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if ((i & 2) == 0) delta_swap<2, 0x33333333u>(x[i], x[i + 2]);
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) delta_swap<1, 0x55555555u>(x[i], x[i + 1]);
+}
+
+template <int W>
+__device__ __forceinline__ void transposeW(uint32_t *x) {
+  if (W == 8) transpose8(x);
+  else transpose16(x);
+}
+
+template <int W>
+__device__ __forceinline__ void load_unit(const uint8_t *p, uint32_t *x) {
+  ldg_v8(p, x);
+  if (W == 16) ldg_v8(p + 32, x + 8);
+}
+template <int W>
+__device__ __forceinline__ void store_unit(uint8_t *p, const uint32_t *x) {
+  stg_v8(p, x);
+  if (W == 16) stg_v8(p + 32, x + 8);
+}
+
+}  // namespace rsb

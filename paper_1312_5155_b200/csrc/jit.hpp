@@ -1,0 +1,57 @@
+// jit.hpp -- run-time specialised bit-sliced kernels (NVRTC, sm_100a).
+//
+// For a fixed GF matrix M (outputs x inputs) -- an erasure pattern's decode
+// matrix R_E = V_E^{-1} A_E (P:244-303 with Opt1/Opt3 of P:319-323 taken to
+// code generation), or the parity map of a code without a compiled network --
+// this builds the GF(2) bit-matrix, reduces it with the same greedy CSE as
+// gen_networks.py and compiles a straight-line kernel: every HBM byte of the
+// n-t survivors read once, the t outputs written once, no runtime tables.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "gf.hpp"
+
+namespace rsb {
+namespace jit {
+
+struct Spec {
+  int w = 8;
+  std::vector<int> in_blk;   // API block indices read, input order
+  std::vector<int> out_blk;  // API block indices written
+  std::vector<uint32_t> M;   // out x in GF(2^w) matrix, row-major
+  int group_blocks = 0;      // inputs per CSE group (0 = all)
+  int min_blocks = 4;        // __launch_bounds__ min CTAs/SM
+};
+
+struct Kernel {
+  bool ok = false;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t fn = nullptr;
+  int xors = 0;
+  double compile_ms = 0;
+  std::string log;
+};
+
+// Argument block of every generated kernel (mirrors the struct in the source).
+struct Args {
+  uint8_t *base;
+  uint64_t stripe_stride, block_stride;
+  const uint64_t *ptrs;
+  int n;
+  int pad;
+  const int32_t *stripes;  // selected stripe indices (nullptr = 0..n_sel-1)
+  uint64_t n_sel, units_per_stripe;
+  uint32_t units_per_cta, ctas_per_stripe;
+};
+
+bool available(std::string *why = nullptr);
+std::string source(const Field &F, const Spec &spec, int *xors);
+Kernel compile(const std::string &src);
+void release(Kernel &k);
+
+}  // namespace jit
+}  // namespace rsb

@@ -11,15 +11,22 @@
 // rewritings of y = V_E^{-1} (D(alpha^0..alpha^{t-1})) -- see DESIGN.md.
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <functional>
+#include <future>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/rs_poly.h"
 #include "gf.hpp"
+#include "jit.hpp"
 #include "rs_kernels.cuh"
 
 using rsb::Field;
@@ -28,6 +35,8 @@ namespace {
 
 struct PatternHost {
   std::vector<int> erased;  // row order of W / R: ascending API index
+  std::vector<int> surv;    // survivors, ascending API index (columns of R)
+  std::vector<uint32_t> R;  // t x (n-t) decode matrix V_E^{-1} A_E
   rsb::SlicedPat sp{};
   std::vector<uint8_t> wtab;  // sliced W tables
   rsb::GenericPat gp{};
@@ -35,6 +44,63 @@ struct PatternHost {
 };
 
 using MaskKey = std::array<uint64_t, 4>;
+
+// A run-time specialised kernel (jit.cpp), compiled once per pattern.
+struct JitEntry {
+  std::shared_future<std::shared_ptr<rsb::jit::Kernel>> fut;
+  bool ready() const { return fut.valid() && fut.wait_for(std::chrono::seconds(0)) == std::future_status::ready; }
+  const rsb::jit::Kernel *kernel() const {
+    if (!ready()) return nullptr;
+    const auto &k = fut.get();
+    return (k && k->ok) ? k.get() : nullptr;
+  }
+};
+
+// Fixed pool of compile workers shared by all plans (NVRTC is thread-safe).
+class CompilePool {
+ public:
+  static CompilePool &get() {
+    static CompilePool p;
+    return p;
+  }
+  void submit(std::function<void()> fn) {
+    std::lock_guard<std::mutex> l(mu_);
+    q_.push_back(std::move(fn));
+    cv_.notify_one();
+  }
+  ~CompilePool() {
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto &t : th_) t.join();
+  }
+
+ private:
+  CompilePool() {
+    unsigned n = std::max(2u, std::min(16u, std::thread::hardware_concurrency()));
+    for (unsigned i = 0; i < n; ++i) th_.emplace_back([this] { run(); });
+  }
+  void run() {
+    for (;;) {
+      std::function<void()> fn;
+      {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [this] { return stop_ || !q_.empty(); });
+        if (q_.empty()) return;
+        fn = std::move(q_.front());
+        q_.pop_front();
+      }
+      fn();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::function<void()>> q_;
+  std::vector<std::thread> th_;
+  bool stop_ = false;
+};
 
 }  // namespace
 
@@ -48,6 +114,22 @@ struct rs_poly_plan {
   std::vector<uint8_t> enc_tab;
   mutable std::mutex mu;
   mutable std::map<MaskKey, std::shared_ptr<const PatternHost>> cache;
+  // run-time specialised kernels: decode patterns (key = erased mask) and, for codes
+  // without a compiled network, the encoder (key = kEncodeKey)
+  int jit_mode = RS_JIT_BACKGROUND;
+  mutable std::map<MaskKey, std::shared_ptr<JitEntry>> jit;
+  mutable std::map<int, std::vector<cudaStream_t>> pool;  // device -> side streams for concurrent launches
+  mutable std::atomic<uint64_t> jit_launches{0}, table_launches{0};
+  ~rs_poly_plan() {
+    for (auto &kv : jit) {
+      if (kv.second->fut.valid()) {
+        auto k = kv.second->fut.get();
+        if (k) rsb::jit::release(*k);
+      }
+    }
+    for (auto &kv : pool)
+      for (cudaStream_t s : kv.second) cudaStreamDestroy(s);
+  }
 };
 
 namespace {
@@ -112,6 +194,8 @@ std::shared_ptr<const PatternHost> build_pattern(const rs_poly_plan &P, const st
       for (int j = 0; j < t; ++j) acc ^= F.mul(V[(size_t)e * t + j], F.alpha_pow((uint64_t)j * p));
       R[(size_t)e * ns + si] = acc;
     }
+  ph->surv = surv;
+  ph->R = R;
   // sliced record
   if (P.sliced) {
     std::memset(&ph->sp, 0, sizeof(ph->sp));
@@ -155,71 +239,155 @@ struct Geometry {
 
 bool ptr_aligned(uint64_t v, uint64_t a) { return (v % a) == 0; }
 
-// Launch encode (pats==nullptr) or decode over a geometry whose constants are in dev blob.
-struct LaunchPlan {
-  // offsets into the device blob
-  size_t pat_idx_off = SIZE_MAX, sliced_pats_off = SIZE_MAX, generic_pats_off = SIZE_MAX, ptrs_off = SIZE_MAX;
-  size_t tables_off = 0;
-  uint32_t generic_groups = 1, generic_smem = 0;
-};
+const MaskKey kEncodeKey{~0ull, ~0ull, ~0ull, ~0ull};
 
-rs_status run_kernels(const rs_poly_plan &P, bool decode, Geometry G, const LaunchPlan &lp, uint8_t *dev,
-                      cudaStream_t st) {
-  if (lp.ptrs_off != SIZE_MAX) G.L.ptrs = reinterpret_cast<const uint64_t *>(dev + lp.ptrs_off);
-  const uint64_t UB = 32ull * (uint64_t)P.w / 8;
-  uint64_t body_units = 0;
-  if (P.sliced && G.aligned32) body_units = G.block_bytes / UB;
-  if (body_units) {
-    rsb::SlicedArgs a{};
-    a.L = G.L;
-    a.n_stripes = G.n_stripes;
-    a.units_per_stripe = body_units;
-    a.units_per_cta = kSlicedUnitsPerCta;
-    a.ctas_per_stripe = (uint32_t)((body_units + kSlicedUnitsPerCta - 1) / kSlicedUnitsPerCta);
-    if (decode) {
-      a.pats = reinterpret_cast<const rsb::SlicedPat *>(dev + lp.sliced_pats_off);
-      a.pat_idx = reinterpret_cast<const int32_t *>(dev + lp.pat_idx_off);
-      a.tables = dev + lp.tables_off;
+bool jit_eligible(const rs_poly_plan &P, int n_out) { return P.w == 8 ? n_out <= 8 : n_out <= 4; }
+
+rsb::jit::Spec jit_spec(const rs_poly_plan &P, const std::vector<int> &in, const std::vector<int> &out,
+                        const std::vector<uint32_t> &M) {
+  rsb::jit::Spec s;
+  s.w = P.w;
+  s.in_blk = in;
+  s.out_blk = out;
+  s.M = M;
+  s.group_blocks = P.w == 8 ? 0 : 3;  // w16: CSE groups of 3 blocks keep the planes in registers
+  s.min_blocks = P.w == 8 ? 4 : 3;
+  return s;
+}
+
+// The compiled kernel for `key` if it is ready; schedules (background) or runs (sync /
+// wait) its compilation on first request.  Must be called without holding P.mu.
+const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const MaskKey &key, const std::function<rsb::jit::Spec()> &mk,
+                                bool wait) {
+  if (P.jit_mode == RS_JIT_OFF || !rsb::jit::available()) return nullptr;
+  std::shared_ptr<JitEntry> e;
+  std::shared_ptr<std::promise<std::shared_ptr<rsb::jit::Kernel>>> prom;
+  {
+    std::lock_guard<std::mutex> lock(P.mu);
+    auto it = P.jit.find(key);
+    if (it != P.jit.end()) {
+      e = it->second;
+    } else {
+      e = std::make_shared<JitEntry>();
+      prom = std::make_shared<std::promise<std::shared_ptr<rsb::jit::Kernel>>>();
+      e->fut = prom->get_future().share();
+      P.jit.emplace(key, e);
     }
-    cudaError_t e = rsb::launch_sliced(P.k, P.m, P.w, P.poly, decode, a, st);
-    if (e != cudaSuccess) return cuda_status(e);
   }
-  const uint64_t col_begin = body_units * UB;
-  if (col_begin < G.block_bytes) {
-    rsb::GenericArgs a{};
-    a.L = G.L;
-    a.pats = reinterpret_cast<const rsb::GenericPat *>(dev + lp.generic_pats_off);
-    a.pat_idx = lp.pat_idx_off == SIZE_MAX ? nullptr : reinterpret_cast<const int32_t *>(dev + lp.pat_idx_off);
-    a.tables = dev + lp.tables_off;
-    a.n_stripes = G.n_stripes;
-    a.col_begin = col_begin;
-    a.col_end = G.block_bytes;
-    const uint64_t span = G.block_bytes - col_begin;
-    const uint64_t step = (uint64_t)kGenericThreads * 16;
-    uint64_t chunk = std::min<uint64_t>(kGenericChunk, (span + step - 1) / step * step);
-    a.chunk_bytes = chunk;
-    a.ctas_per_group = (uint32_t)((span + chunk - 1) / chunk);
-    a.n_groups = lp.generic_groups;
-    a.vec_ok = G.aligned16 ? 1u : 0u;
-    a.smem_bytes = lp.generic_smem;
-    cudaError_t e = rsb::launch_generic(P.w, a, st);
-    if (e != cudaSuccess) return cuda_status(e);
+  const bool block = wait || P.jit_mode == RS_JIT_SYNC;
+  if (prom) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto job = [prom, spec = mk(), F = &P.F, dev]() {
+      cudaSetDevice(dev);  // load the module under the caller's device, not device 0
+      int xors = 0;
+      const std::string src = rsb::jit::source(*F, spec, &xors);
+      auto k = std::make_shared<rsb::jit::Kernel>(rsb::jit::compile(src));
+      k->xors = xors;
+      prom->set_value(k);
+    };
+    if (block) job();
+    else CompilePool::get().submit(job);
   }
-  return RS_OK;
+  if (block) e->fut.wait();
+  return e->kernel();
 }
 
-// Upload a blob and run; the blob is freed stream-ordered after the kernels.
-rs_status upload_and_run(const rs_poly_plan &P, bool decode, const Geometry &G, const LaunchPlan &lp, Blob &b,
-                         cudaStream_t st) {
-  void *dev = nullptr;
-  cudaError_t e = cudaMallocAsync(&dev, std::max<size_t>(b.h.size(), 16), st);
-  if (e != cudaSuccess) return cuda_status(e);
-  e = cudaMemcpyAsync(dev, b.h.data(), b.h.size(), cudaMemcpyHostToDevice, st);
-  rs_status rc = e == cudaSuccess ? run_kernels(P, decode, G, lp, static_cast<uint8_t *>(dev), st) : cuda_status(e);
-  cudaError_t ef = cudaFreeAsync(dev, st);
-  if (rc == RS_OK && ef != cudaSuccess) rc = cuda_status(ef);
-  return rc;
+std::vector<cudaStream_t> side_streams(const rs_poly_plan &P) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(P.mu);
+  auto &v = P.pool[dev];
+  while (v.size() < 3) {
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) break;
+    v.push_back(s);
+  }
+  return v;
 }
+
+uint64_t body_units_of(const rs_poly_plan &P, const Geometry &G) {
+  const uint64_t UB = 32ull * (uint64_t)P.w / 8;
+  return G.aligned32 ? G.block_bytes / UB : 0;
+}
+
+cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32_t *stripes, uint64_t n_sel,
+                       uint64_t body_units, cudaStream_t st) {
+  rsb::jit::Args a{};
+  a.base = G.L.base;
+  a.stripe_stride = G.L.stripe_stride;
+  a.block_stride = G.L.block_stride;
+  a.ptrs = G.L.ptrs;
+  a.n = G.L.n;
+  a.stripes = stripes;
+  a.n_sel = n_sel;
+  a.units_per_stripe = body_units;
+  a.units_per_cta = kSlicedUnitsPerCta;
+  a.ctas_per_stripe = (uint32_t)((body_units + kSlicedUnitsPerCta - 1) / kSlicedUnitsPerCta);
+  const uint64_t grid = n_sel * a.ctas_per_stripe;
+  if (grid == 0) return cudaSuccess;
+  if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+  void *args[] = {&a};
+  rsb::count_launch();
+  return cudaLaunchKernel(reinterpret_cast<const void *>(k.fn), dim3((unsigned)grid), dim3(kSlicedThreads), args, 0,
+                          st);
+}
+
+cudaError_t launch_sliced_body(const rs_poly_plan &P, bool decode, const Geometry &G, uint64_t body_units,
+                               const uint8_t *dev, size_t pats_off, size_t idx_off, size_t tables_off,
+                               cudaStream_t st) {
+  rsb::SlicedArgs a{};
+  a.L = G.L;
+  a.n_stripes = G.n_stripes;
+  a.units_per_stripe = body_units;
+  a.units_per_cta = kSlicedUnitsPerCta;
+  a.ctas_per_stripe = (uint32_t)((body_units + kSlicedUnitsPerCta - 1) / kSlicedUnitsPerCta);
+  if (decode) {
+    a.pats = reinterpret_cast<const rsb::SlicedPat *>(dev + pats_off);
+    a.pat_idx = reinterpret_cast<const int32_t *>(dev + idx_off);
+    a.tables = dev + tables_off;
+  }
+  return rsb::launch_sliced(P.k, P.m, P.w, P.poly, decode, a, st);
+}
+
+cudaError_t launch_generic_range(const rs_poly_plan &P, const Geometry &G, uint64_t col_begin, uint64_t col_end,
+                                 const uint8_t *dev, size_t pats_off, size_t idx_off, size_t tables_off,
+                                 uint32_t groups, uint32_t smem, cudaStream_t st) {
+  if (col_begin >= col_end) return cudaSuccess;
+  rsb::GenericArgs a{};
+  a.L = G.L;
+  a.pats = reinterpret_cast<const rsb::GenericPat *>(dev + pats_off);
+  a.pat_idx = idx_off == SIZE_MAX ? nullptr : reinterpret_cast<const int32_t *>(dev + idx_off);
+  a.tables = dev + tables_off;
+  a.n_stripes = G.n_stripes;
+  a.col_begin = col_begin;
+  a.col_end = col_end;
+  const uint64_t span = col_end - col_begin;
+  const uint64_t step = (uint64_t)kGenericThreads * 16;
+  const uint64_t chunk = std::min<uint64_t>(kGenericChunk, (span + step - 1) / step * step);
+  a.chunk_bytes = chunk;
+  a.ctas_per_group = (uint32_t)((span + chunk - 1) / chunk);
+  a.n_groups = groups;
+  a.vec_ok = G.aligned16 ? 1u : 0u;
+  a.smem_bytes = smem;
+  return rsb::launch_generic(P.w, a, st);
+}
+
+struct DevBlob {
+  uint8_t *p = nullptr;
+  cudaStream_t st = nullptr;
+  cudaError_t upload(const Blob &b, cudaStream_t s) {
+    st = s;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p), std::max<size_t>(b.h.size(), 16), s);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(p, b.h.data(), b.h.size(), cudaMemcpyHostToDevice, s);
+  }
+  cudaError_t release() {
+    cudaError_t e = p ? cudaFreeAsync(p, st) : cudaSuccess;
+    p = nullptr;
+    return e;
+  }
+};
 
 rs_status check_geometry(const rs_poly_plan *P, size_t block_bytes) {
   if (!P) return RS_ERR_INVALID_ARG;
@@ -228,78 +396,188 @@ rs_status check_geometry(const rs_poly_plan *P, size_t block_bytes) {
 }
 
 rs_status encode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs, cudaStream_t st) {
+  const rsb::jit::Kernel *jk = nullptr;
+  uint64_t body = body_units_of(*P, G);
+  if (body && !P->sliced && jit_eligible(*P, P->m)) {
+    std::vector<int> in(P->k), out(P->m);
+    for (int j = 0; j < P->k; ++j) in[j] = j;
+    for (int i = 0; i < P->m; ++i) out[i] = P->k + i;
+    jk = jit_get(*P, kEncodeKey, [&] { return jit_spec(*P, in, out, P->pmap); }, false);
+  }
+  if (!P->sliced && !jk) body = 0;
   Blob b;
-  LaunchPlan lp;
-  if (ptrs) lp.ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
-  lp.generic_pats_off = b.add(&P->enc_gp, sizeof(P->enc_gp));
-  lp.tables_off = b.add(P->enc_tab.data(), P->enc_tab.size());
+  size_t ptrs_off = SIZE_MAX;
+  if (ptrs) ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
   rsb::GenericPat gp = P->enc_gp;
   gp.table_off = 0;
-  std::memcpy(b.h.data() + lp.generic_pats_off, &gp, sizeof(gp));
-  lp.generic_groups = (uint32_t)((P->m + 3) / 4);
-  lp.generic_smem = (uint32_t)(P->k * (P->w == 8 ? 128 : 512));
-  return upload_and_run(*P, false, G, lp, b, st);
+  const size_t pats_off = b.add(&gp, sizeof(gp));
+  const size_t tables_off = b.add(P->enc_tab.data(), P->enc_tab.size());
+  DevBlob d;
+  cudaError_t e = d.upload(b, st);
+  if (e == cudaSuccess && ptrs) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
+  if (e == cudaSuccess && body) {
+    if (P->sliced) {
+      e = launch_sliced_body(*P, false, G, body, d.p, 0, 0, 0, st);
+    } else {
+      e = launch_jit(*jk, G, nullptr, G.n_stripes, body, st);
+      P->jit_launches++;
+    }
+  }
+  const uint64_t UB = 32ull * (uint64_t)P->w / 8;
+  if (e == cudaSuccess)
+    e = launch_generic_range(*P, G, body * UB, G.block_bytes, d.p, pats_off, SIZE_MAX, tables_off,
+                             (uint32_t)((P->m + 3) / 4), (uint32_t)(P->k * (P->w == 8 ? 128 : 512)), st);
+  cudaError_t ef = d.release();
+  return cuda_status(e != cudaSuccess ? e : ef);
+}
+
+// Distinct patterns of a batch, in order of first appearance, with each stripe's index.
+rs_status collect_patterns(const rs_poly_plan *P, const std::vector<std::vector<int>> &rows,
+                           std::vector<std::shared_ptr<const PatternHost>> &pats, std::vector<MaskKey> &keys,
+                           std::vector<int32_t> &idx) {
+  std::map<MaskKey, int> local;
+  idx.assign(rows.size(), -1);
+  std::lock_guard<std::mutex> lock(P->mu);
+  for (size_t s = 0; s < rows.size(); ++s) {
+    const auto &er = rows[s];
+    if (er.empty()) continue;
+    MaskKey key{0, 0, 0, 0};
+    for (int b : er) key[b >> 6] |= 1ull << (b & 63);
+    auto it = local.find(key);
+    if (it != local.end()) {
+      idx[s] = it->second;
+      continue;
+    }
+    auto c = P->cache.find(key);
+    std::shared_ptr<const PatternHost> ph;
+    if (c != P->cache.end()) {
+      ph = c->second;
+    } else {
+      ph = build_pattern(*P, er);
+      if (!ph) return RS_ERR_INVALID_ARG;
+      P->cache.emplace(key, ph);
+    }
+    idx[s] = (int32_t)pats.size();
+    local.emplace(key, (int)pats.size());
+    pats.push_back(ph);
+    keys.push_back(key);
+  }
+  return RS_OK;
+}
+
+const rsb::jit::Kernel *pattern_jit(const rs_poly_plan &P, const PatternHost &ph, const MaskKey &key, bool wait) {
+  if (!jit_eligible(P, (int)ph.erased.size())) return nullptr;
+  return jit_get(P, key, [&] { return jit_spec(P, ph.surv, ph.erased, ph.R); }, wait);
 }
 
 // rows: per stripe list of erased API indices (validated, sorted ascending)
 rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
                       const std::vector<std::vector<int>> &rows, cudaStream_t st) {
-  // distinct patterns
   std::vector<std::shared_ptr<const PatternHost>> pats;
-  std::map<MaskKey, int> local;
-  std::vector<int32_t> idx(G.n_stripes, -1);
-  bool any = false;
-  {
-    std::lock_guard<std::mutex> lock(P->mu);
-    for (uint64_t s = 0; s < G.n_stripes; ++s) {
-      const auto &er = rows[s];
-      if (er.empty()) continue;
-      MaskKey key{0, 0, 0, 0};
-      for (int b : er) key[b >> 6] |= 1ull << (b & 63);
-      auto it = local.find(key);
-      if (it != local.end()) { idx[s] = it->second; any = true; continue; }
-      auto c = P->cache.find(key);
-      std::shared_ptr<const PatternHost> ph;
-      if (c != P->cache.end()) {
-        ph = c->second;
-      } else {
-        ph = build_pattern(*P, er);
-        if (!ph) return RS_ERR_INVALID_ARG;
-        P->cache.emplace(key, ph);
-      }
-      idx[s] = (int)pats.size();
-      local.emplace(key, (int)pats.size());
-      pats.push_back(ph);
-      any = true;
+  std::vector<MaskKey> keys;
+  std::vector<int32_t> idx;
+  rs_status rc = collect_patterns(P, rows, pats, keys, idx);
+  if (rc) return rc;
+  if (pats.empty()) return RS_OK;
+  const uint64_t UB = 32ull * (uint64_t)P->w / 8;
+  uint64_t body = body_units_of(*P, G);
+  // JIT kernels for the patterns whose compile is done (others fall back to tables)
+  std::vector<const rsb::jit::Kernel *> jk(pats.size(), nullptr);
+  bool any_jit = false;
+  if (body)
+    for (size_t i = 0; i < pats.size(); ++i) {
+      jk[i] = pattern_jit(*P, *pats[i], keys[i], false);
+      any_jit = any_jit || jk[i];
+    }
+  if (!P->sliced && !any_jit) body = 0;
+  std::vector<int32_t> idx_rt(idx);
+  std::vector<std::vector<int32_t>> groups(pats.size());
+  bool any_rt = false;
+  for (size_t s = 0; s < idx.size(); ++s) {
+    if (idx[s] < 0) continue;
+    if (jk[idx[s]]) {
+      groups[idx[s]].push_back((int32_t)s);
+      idx_rt[s] = -1;
+    } else {
+      any_rt = true;
     }
   }
-  if (!any) return RS_OK;
   Blob b;
-  LaunchPlan lp;
-  if (ptrs) lp.ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
-  lp.pat_idx_off = b.add(idx.data(), sizeof(int32_t) * idx.size());
+  size_t ptrs_off = SIZE_MAX;
+  if (ptrs) ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
+  const size_t idx_off = b.add(idx.data(), sizeof(int32_t) * idx.size());
+  const size_t idx_rt_off = b.add(idx_rt.data(), sizeof(int32_t) * idx_rt.size());
+  std::vector<size_t> grp_off(pats.size(), SIZE_MAX);
+  for (size_t i = 0; i < pats.size(); ++i)
+    if (!groups[i].empty()) grp_off[i] = b.add(groups[i].data(), sizeof(int32_t) * groups[i].size());
   std::vector<rsb::SlicedPat> sps(pats.size());
   std::vector<rsb::GenericPat> gps(pats.size());
-  lp.sliced_pats_off = b.add(nullptr, sizeof(rsb::SlicedPat) * sps.size());
-  lp.generic_pats_off = b.add(nullptr, sizeof(rsb::GenericPat) * gps.size());
-  lp.tables_off = b.add(nullptr, 0);
+  const size_t sliced_pats_off = b.add(nullptr, sizeof(rsb::SlicedPat) * sps.size());
+  const size_t generic_pats_off = b.add(nullptr, sizeof(rsb::GenericPat) * gps.size());
+  const size_t tables_off = b.add(nullptr, 0);
   uint32_t max_groups = 1, max_in = 1;
   for (size_t i = 0; i < pats.size(); ++i) {
     const PatternHost &ph = *pats[i];
     if (P->sliced) {
       sps[i] = ph.sp;
-      sps[i].table_off = (uint32_t)(b.add(ph.wtab.data(), ph.wtab.size()) - lp.tables_off);
+      sps[i].table_off = (uint32_t)(b.add(ph.wtab.data(), ph.wtab.size()) - tables_off);
     }
     gps[i] = ph.gp;
-    gps[i].table_off = (uint32_t)(b.add(ph.rtab.data(), ph.rtab.size()) - lp.tables_off);
+    gps[i].table_off = (uint32_t)(b.add(ph.rtab.data(), ph.rtab.size()) - tables_off);
     max_groups = std::max<uint32_t>(max_groups, (uint32_t)((ph.gp.n_out + 3) / 4));
     max_in = std::max<uint32_t>(max_in, (uint32_t)ph.gp.n_in);
   }
-  std::memcpy(b.h.data() + lp.sliced_pats_off, sps.data(), sizeof(rsb::SlicedPat) * sps.size());
-  std::memcpy(b.h.data() + lp.generic_pats_off, gps.data(), sizeof(rsb::GenericPat) * gps.size());
-  lp.generic_groups = max_groups;
-  lp.generic_smem = max_in * (P->w == 8 ? 128 : 512);
-  return upload_and_run(*P, true, G, lp, b, st);
+  std::memcpy(b.h.data() + sliced_pats_off, sps.data(), sizeof(rsb::SlicedPat) * sps.size());
+  std::memcpy(b.h.data() + generic_pats_off, gps.data(), sizeof(rsb::GenericPat) * gps.size());
+  const uint32_t smem = max_in * (P->w == 8 ? 128 : 512);
+
+  DevBlob d;
+  cudaError_t e = d.upload(b, st);
+  if (e == cudaSuccess && ptrs) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
+  // table-driven body for stripes without a ready JIT kernel
+  if (e == cudaSuccess && body && any_rt) {
+    if (P->sliced) e = launch_sliced_body(*P, true, G, body, d.p, sliced_pats_off, idx_rt_off, tables_off, st);
+    else e = launch_generic_range(*P, G, 0, body * UB, d.p, generic_pats_off, idx_rt_off, tables_off, max_groups,
+                                  smem, st);
+    P->table_launches++;
+  }
+  // ragged tails (and everything when there is no bit-sliced body)
+  if (e == cudaSuccess)
+    e = launch_generic_range(*P, G, body * UB, G.block_bytes, d.p, generic_pats_off, idx_off, tables_off,
+                             max_groups, smem, st);
+  // JIT kernels, one launch per pattern, spread over side streams so short launches overlap
+  if (e == cudaSuccess && any_jit) {
+    std::vector<cudaStream_t> side = side_streams(*P);
+    cudaEvent_t fork = nullptr;
+    e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(fork, st);
+    std::vector<char> used(side.size(), 0);
+    size_t rr = 0;
+    for (size_t i = 0; i < pats.size() && e == cudaSuccess; ++i) {
+      if (groups[i].empty()) continue;
+      const size_t lane = rr++ % (side.size() + 1);
+      cudaStream_t s = lane == 0 ? st : side[lane - 1];
+      if (lane && !used[lane - 1]) {
+        e = cudaStreamWaitEvent(s, fork, 0);
+        used[lane - 1] = 1;
+      }
+      if (e == cudaSuccess)
+        e = launch_jit(*jk[i], G, reinterpret_cast<const int32_t *>(d.p + grp_off[i]), groups[i].size(), body, s);
+      P->jit_launches++;
+    }
+    for (size_t l = 0; l < side.size(); ++l) {
+      if (!used[l]) continue;
+      cudaEvent_t join = nullptr;
+      cudaError_t e2 = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+      if (e2 == cudaSuccess) e2 = cudaEventRecord(join, side[l]);
+      if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, join, 0);
+      if (join) cudaEventDestroy(join);
+      if (e == cudaSuccess) e = e2;
+    }
+    if (fork) cudaEventDestroy(fork);
+  }
+  cudaError_t ef = d.release();
+  return cuda_status(e != cudaSuccess ? e : ef);
 }
 
 rs_status parse_row(const rs_poly_plan *P, const int32_t *row, int count, std::vector<int> &out, bool allow_pad) {
@@ -394,6 +672,85 @@ rs_status rs_poly_plan_create(int k, int m, int w, uint32_t prim_poly, rs_poly_p
 }
 
 void rs_poly_plan_destroy(rs_poly_plan *plan) { delete plan; }
+
+rs_status rs_poly_plan_set_jit(rs_poly_plan *P, int mode) {
+  if (!P || mode < RS_JIT_OFF || mode > RS_JIT_SYNC) return RS_ERR_INVALID_ARG;
+  P->jit_mode = mode;
+  return RS_OK;
+}
+
+rs_status rs_poly_prepare(const rs_poly_plan *P, const int32_t *erasures, size_t n_rows) {
+  if (!P || (n_rows && !erasures)) return RS_ERR_INVALID_ARG;
+  std::vector<std::vector<int>> rows(n_rows);
+  for (size_t s = 0; s < n_rows; ++s) {
+    rs_status rc = parse_row(P, erasures + s * (size_t)P->m, P->m, rows[s], true);
+    if (rc) return rc;
+  }
+  std::vector<std::shared_ptr<const PatternHost>> pats;
+  std::vector<MaskKey> keys;
+  std::vector<int32_t> idx;
+  rs_status rc = collect_patterns(P, rows, pats, keys, idx);
+  if (rc) return rc;
+  if (P->jit_mode == RS_JIT_OFF) return RS_OK;
+  if (!P->sliced && jit_eligible(*P, P->m)) {
+    std::vector<int> in(P->k), out(P->m);
+    for (int j = 0; j < P->k; ++j) in[j] = j;
+    for (int i = 0; i < P->m; ++i) out[i] = P->k + i;
+    jit_get(*P, kEncodeKey, [&] { return jit_spec(*P, in, out, P->pmap); }, false);
+  }
+  for (size_t i = 0; i < pats.size(); ++i) pattern_jit(*P, *pats[i], keys[i], false);  // queue all first
+  std::vector<std::shared_ptr<JitEntry>> wait;
+  {
+    std::lock_guard<std::mutex> lock(P->mu);
+    for (auto &kv : P->jit) wait.push_back(kv.second);
+  }
+  for (auto &e : wait)
+    if (e->fut.valid()) e->fut.wait();
+  return RS_OK;
+}
+
+size_t rs_poly_jit_source(const rs_poly_plan *P, const int *erasures, int n_erasures, char *buf, size_t cap) {
+  if (!P || n_erasures < 0 || n_erasures > P->m || (n_erasures && !erasures)) return 0;
+  rsb::jit::Spec spec;
+  if (n_erasures == 0) {
+    if (!jit_eligible(*P, P->m)) return 0;
+    std::vector<int> in(P->k), out(P->m);
+    for (int j = 0; j < P->k; ++j) in[j] = j;
+    for (int i = 0; i < P->m; ++i) out[i] = P->k + i;
+    spec = jit_spec(*P, in, out, P->pmap);
+  } else {
+    std::vector<int32_t> row(erasures, erasures + n_erasures);
+    std::vector<int> er;
+    if (parse_row(P, row.data(), n_erasures, er, false) || !jit_eligible(*P, (int)er.size())) return 0;
+    auto ph = build_pattern(*P, er);
+    if (!ph) return 0;
+    spec = jit_spec(*P, ph->surv, ph->erased, ph->R);
+  }
+  const std::string s = rsb::jit::source(P->F, spec, nullptr);
+  if (buf && cap) {
+    const size_t nc = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), nc);
+    buf[nc] = 0;
+  }
+  return s.size();
+}
+
+rs_status rs_poly_plan_stats(const rs_poly_plan *P, rs_poly_stats *out) {
+  if (!P || !out) return RS_ERR_INVALID_ARG;
+  std::memset(out, 0, sizeof(*out));
+  std::lock_guard<std::mutex> lock(P->mu);
+  out->patterns = P->cache.size();
+  for (auto &kv : P->jit) {
+    if (!kv.second->ready()) out->jit_pending++;
+    else if (kv.second->kernel()) out->jit_ready++;
+    else out->jit_failed++;
+  }
+  out->jit_launches = P->jit_launches.load();
+  out->table_launches = P->table_launches.load();
+  out->jit_available = rsb::jit::available() ? 1 : 0;
+  out->jit_mode = P->jit_mode;
+  return RS_OK;
+}
 
 rs_status rs_poly_plan_info(const rs_poly_plan *P, uint32_t *g_out, uint32_t *pmap_out) {
   if (!P) return RS_ERR_INVALID_ARG;

@@ -37,6 +37,23 @@ _lib.rs_poly_decode_host.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _vp, _P(
 _lib.rs_poly_strerror.argtypes = [_i32]
 _lib.rs_poly_strerror.restype = ctypes.c_char_p
 _lib.rs_poly_abi_version.restype = _i32
+_lib.rs_poly_plan_set_jit.argtypes = [_vp, _i32]
+_lib.rs_poly_prepare.argtypes = [_vp, _vp, _sz]
+_lib.rs_poly_plan_stats.argtypes = [_vp, _vp]
+_lib.rs_poly_jit_source.argtypes = [_vp, _vp, _i32, ctypes.c_char_p, _sz]
+_lib.rs_poly_jit_source.restype = _sz
+
+
+class Stats(ctypes.Structure):
+    """rs_poly_stats"""
+    _fields_ = [("patterns", _u64), ("jit_ready", _u64), ("jit_pending", _u64), ("jit_failed", _u64),
+                ("jit_launches", _u64), ("table_launches", _u64), ("jit_available", _i32), ("jit_mode", _i32)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+RS_JIT_OFF, RS_JIT_BACKGROUND, RS_JIT_SYNC = 0, 1, 2
 _lib.rs_poly_launch_count.restype = _u64
 
 RS_OK, RS_ERR_INVALID_ARG, RS_ERR_NOT_PRIMITIVE, RS_ERR_GEOMETRY = 0, 1, 2, 3
@@ -134,6 +151,32 @@ class Plan:
 
     def __exit__(self, *exc):
         self.close()
+
+    # ---- run-time specialised kernels ------------------------------------------
+    def set_jit(self, mode: int) -> None:
+        """RS_JIT_OFF / RS_JIT_BACKGROUND (default) / RS_JIT_SYNC."""
+        _check(_lib.rs_poly_plan_set_jit(self._h, mode), "rs_poly_plan_set_jit")
+
+    def prepare(self, erasures) -> None:
+        """Precompute decode constants and compile JIT kernels for these patterns ([rows][m], -1 padded)."""
+        er = np.ascontiguousarray(np.asarray(erasures, dtype=np.int32)).reshape(-1, self.m)
+        _check(_lib.rs_poly_prepare(self._h, er.ctypes.data, er.shape[0]), "rs_poly_prepare")
+
+    def stats(self) -> dict:
+        st = Stats()
+        _check(_lib.rs_poly_plan_stats(self._h, ctypes.byref(st)), "rs_poly_plan_stats")
+        return st.as_dict()
+
+    def jit_source(self, erasures=()) -> str:
+        """CUDA source the JIT generates for an erasure list (empty = the encoder); '' if not eligible."""
+        er = list(erasures)
+        e = (ctypes.c_int * max(1, len(er)))(*er)
+        n = _lib.rs_poly_jit_source(self._h, e, len(er), None, 0)
+        if n == 0:
+            return ""
+        buf = ctypes.create_string_buffer(n + 1)
+        _lib.rs_poly_jit_source(self._h, e, len(er), buf, n + 1)
+        return buf.value.decode()
 
     @property
     def kernel_kind(self) -> str:

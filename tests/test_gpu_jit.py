@@ -1,0 +1,108 @@
+"""GPU parity of the run-time specialised (NVRTC) kernels vs the CPU oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+P8, P16 = 0x11D, 0x1100B
+
+
+def rs():
+    import paper_1312_5155_b200 as m
+    return m
+
+
+def encoded(k, m, w, poly, B, S, seed):
+    st = synth.stripes_array(seed, range(S), k, m, B)
+    oracle.encode_bulk(st, k, m, w, poly, threads=8)
+    return st
+
+
+@pytest.mark.parametrize("k,m,w,poly,B", [(10, 4, 8, P8, 64 * 1024 + 40), (12, 4, 16, P16, 32 * 1024 + 6),
+                                          (6, 3, 8, P8, 8192), (5, 2, 8, P8, 4096 + 3), (10, 6, 8, P8, 2048)])
+def test_jit_decode_matches_oracle(k, m, w, poly, B):
+    S, n = 12, k + m
+    ref = encoded(k, m, w, poly, B, S, seed=21)
+    rng = np.random.default_rng(k + 100 * m)
+    er = np.full((S, m), -1, dtype=np.int32)
+    for s in range(S):
+        t = [m, 1, m][s] if s < 3 else int(rng.integers(1, m + 1))
+        er[s, :t] = rng.choice(n, t, replace=False)
+    er[5] = er[4]  # two stripes sharing a pattern -> one launch covers both
+    bad = ref.copy()
+    for s in range(S):
+        for b in er[s]:
+            if b >= 0:
+                bad[s, b] = 0x3C
+    m_ = rs()
+    plan = m_.Plan(k, m, w, poly)
+    plan.set_jit(m_.RS_JIT_SYNC)
+    d = torch.from_numpy(bad).cuda()
+    plan.decode_batch(d, er)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    st = plan.stats()
+    assert st["jit_available"] == 1 and st["jit_failed"] == 0
+    eligible = any((er[s] >= 0).sum() <= (8 if w == 8 else 4) for s in range(S))
+    assert (st["jit_launches"] > 0) == eligible
+
+
+def test_prepare_then_decode_uses_only_jit():
+    k, m, B, S = 10, 4, 256 * 1024, 16
+    ref = encoded(k, m, 8, P8, B, S, seed=22)
+    er = synth.erasure_table("C5", 3, S)
+    m_ = rs()
+    plan = m_.Plan(k, m)
+    plan.prepare(er)
+    st = plan.stats()
+    assert st["jit_ready"] == len({tuple(r) for r in er.tolist()}) and st["jit_pending"] == 0
+    bad = ref.copy()
+    for s in range(S):
+        bad[s, er[s]] = 0
+    d = torch.from_numpy(bad).cuda()
+    plan.decode_batch(d, er)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    st2 = plan.stats()
+    assert st2["table_launches"] == 0 and st2["jit_launches"] == st["jit_ready"]
+
+
+def test_background_mode_converges():
+    """Background JIT: first calls use tables, later ones the compiled kernels; always exact."""
+    import time
+    k, m, B, S = 6, 3, 64 * 1024, 4
+    ref = encoded(k, m, 8, P8, B, S, seed=23)
+    er = np.array([[0, 2, 7], [1, -1, -1], [6, 7, 8], [0, 2, 7]], dtype=np.int32)
+    m_ = rs()
+    plan = m_.Plan(k, m)
+    d = torch.from_numpy(ref).cuda()
+    for it in range(60):
+        for s in range(S):
+            d[s, torch.from_numpy(er[s][er[s] >= 0].astype(np.int64)).cuda()] = 0
+        plan.decode_batch(d, er)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy(), ref)
+        st = plan.stats()
+        if st["jit_pending"] == 0 and st["jit_launches"] > 0:
+            break
+        time.sleep(0.1)
+    assert st["jit_ready"] == 3 and st["jit_launches"] > 0
+
+
+@pytest.mark.parametrize("k,m,w,poly", [(5, 2, 8, P8), (10, 4, 16, P16)])
+def test_jit_encoder_for_codes_without_compiled_network(k, m, w, poly):
+    B, S = 8192 + 64, 3
+    ref = encoded(k, m, w, poly, B, S, seed=24)
+    m_ = rs()
+    plan = m_.Plan(k, m, w, poly)
+    assert plan.kernel_kind == "generic"
+    plan.set_jit(m_.RS_JIT_SYNC)
+    d = torch.from_numpy(ref).cuda()
+    d[:, k:] = 0
+    plan.encode_batch(d)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    assert plan.stats()["jit_launches"] == 1

@@ -19,9 +19,24 @@ pytestmark = pytest.mark.gpu
 P8, P16 = 0x11D, 0x1100B
 
 
+class _TablesOnly:
+    """The table-driven / compiled-network kernels (JIT off); tests/test_gpu_jit.py covers the JIT path."""
+
+    def __init__(self, mod):
+        self._m = mod
+
+    def __getattr__(self, name):
+        return getattr(self._m, name)
+
+    def Plan(self, *a, **kw):
+        p = self._m.Plan(*a, **kw)
+        p.set_jit(self._m.RS_JIT_OFF)
+        return p
+
+
 def rs():
     import paper_1312_5155_b200 as m
-    return m
+    return _TablesOnly(m)
 
 
 def host_stripes(k, m, B, S, seed=0, stripe0=0):

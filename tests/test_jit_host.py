@@ -1,0 +1,138 @@
+"""The run-time generated (JIT) kernels, checked on the CPU.
+
+rs_poly_jit_source returns the CUDA source the library would compile for an erasure
+pattern (or for the encoder of a code without a compiled network).  Here its XOR
+network is parsed and evaluated on random columns (as bit-planes) and compared with
+the CPU oracle's decode/encode; one source per field is also compiled with nvcc for
+sm_100a.  The GPU-side parity of the compiled kernels is in tests/test_gpu_jit.py.
+"""
+import os
+import re
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+import oracle
+
+P8, P16 = 0x11D, 0x1100B
+
+
+@pytest.fixture(scope="module")
+def rs():
+    import paper_1312_5155_b200 as m
+    return m
+
+
+def parse(src):
+    ins = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bi(\d+) = blkp\(a, s, (\d+)\);", src)}
+    outs = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bo(\d+) = blkp\(a, s, (\d+)\);", src)}
+    w = int(re.search(r"const uint64_t off = u \* (\d+)ull;", src).group(1)) * 8 // 32
+    groups = []
+    for body in re.findall(r"^    \{\n(.*?)\n    \}$", src, re.S | re.M):
+        loads = [(int(i), int(base)) for i, base in re.findall(r"load_unit<\d+>\(bi(\d+) \+ off, &x\[(\d+)\]\);", body)]
+        stmts = re.findall(r"^\s+(const uint32_t (t\d+)|y\[(\d+)\]) (\^?=) (.*);$", body, re.M)
+        groups.append((loads, stmts))
+    stores = [(int(i), int(base)) for i, base in re.findall(r"store_unit<\d+>\(bo(\d+) \+ off, &y\[(\d+)\]\);", src)]
+    return w, ins, outs, groups, stores
+
+
+def evaluate(src, cw_cols):
+    """cw_cols: [n][C] symbols (API order).  Returns {out_block: [C] symbols}."""
+    w, ins, outs, groups, stores = parse(src)
+    C = cw_cols.shape[1]
+    nout = len(outs)
+    y = [0] * (nout * w)
+    for loads, stmts in groups:
+        x = {}
+        for i, base in loads:
+            blk = ins[i]
+            for b in range(w):
+                x[base + b] = sum(((int(cw_cols[blk][c]) >> b) & 1) << c for c in range(C))
+        env = {}
+
+        def val(tok):
+            tok = tok.strip()
+            if tok.startswith("x["):
+                return x[int(tok[2:-1])]
+            if tok == "0u":
+                return 0
+            return env[tok]
+
+        for _, tname, yidx, op, expr in stmts:
+            v = 0
+            for tok in expr.split("^"):
+                v ^= val(tok)
+            if tname:
+                env[tname] = v
+            elif op == "=":
+                y[int(yidx)] = v
+            else:
+                y[int(yidx)] ^= v
+    res = {}
+    for i, base in stores:
+        res[outs[i]] = [sum(((y[base + o] >> c) & 1) << o for o in range(w)) for c in range(C)]
+    return res
+
+
+def codewords(k, m, w, poly, C, seed):
+    rng = np.random.default_rng(seed)
+    cols = np.zeros((k + m, C), dtype=np.int64)
+    for c in range(C):
+        d = [int(v) for v in rng.integers(0, 1 << w, k)]
+        cols[:, c] = d + oracle.encode_column(d, m, w, poly)
+    return cols
+
+
+@pytest.mark.parametrize("k,m,w,poly", [(10, 4, 8, P8), (6, 3, 8, P8), (12, 4, 16, P16), (5, 2, 8, P8),
+                                        (10, 6, 8, P8), (20, 8, 8, P8)])
+def test_jit_decode_networks_match_oracle(rs, k, m, w, poly):
+    plan = rs.Plan(k, m, w, poly)
+    n = k + m
+    rng = np.random.default_rng(k * 31 + m)
+    cols = codewords(k, m, w, poly, 32, seed=k + m)
+    pats = [list(range(m)), list(range(k, n)), [0, n - 1][: min(2, m)], [k - 1]]
+    for _ in range(6):
+        t = int(rng.integers(1, m + 1))
+        pats.append(sorted(rng.choice(n, t, replace=False).tolist()))
+    for er in pats:
+        src = plan.jit_source(er)
+        eligible = len(er) <= (8 if w == 8 else 4)
+        assert bool(src) == eligible
+        if not src:
+            continue
+        got = evaluate(src, cols)
+        assert sorted(got) == sorted(er)
+        for b in er:
+            assert got[b] == [int(v) for v in cols[b]], (er, b)
+
+
+@pytest.mark.parametrize("k,m,w,poly", [(5, 2, 8, P8), (10, 6, 8, P8), (10, 4, 16, P16), (3, 1, 8, P8)])
+def test_jit_encoder_matches_oracle(rs, k, m, w, poly):
+    plan = rs.Plan(k, m, w, poly)
+    src = plan.jit_source([])
+    assert src
+    cols = codewords(k, m, w, poly, 32, seed=5)
+    got = evaluate(src, cols)
+    for i in range(m):
+        assert got[k + i] == [int(v) for v in cols[k + i]]
+
+
+def test_jit_not_eligible_when_too_many_outputs(rs):
+    assert rs.Plan(10, 6, 16, P16).jit_source([0, 1, 2, 3, 4]) == ""   # w16: at most 4 outputs
+    assert rs.Plan(20, 9, 8, P8).jit_source([]) == ""                  # w8: at most 8 outputs
+    assert rs.Plan(10, 4).jit_source([0, 0]) == ""                      # invalid list
+
+
+@pytest.mark.parametrize("k,m,w,poly,er", [(10, 4, 8, P8, [1, 4, 10, 13]), (12, 4, 16, P16, [0, 5, 12, 15])])
+def test_jit_source_compiles_for_sm100a(rs, k, m, w, poly, er):
+    src = rs.Plan(k, m, w, poly).jit_source(er)
+    with tempfile.TemporaryDirectory() as d:
+        f = os.path.join(d, "jit.cu")
+        open(f, "w").write(src)
+        out = subprocess.run(["/usr/local/cuda/bin/nvcc", "-cubin", "-gencode", "arch=compute_100a,code=sm_100a",
+                              "-std=c++17", "-Xptxas", "-v", "-o", os.path.join(d, "jit.cubin"), f],
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-3000:]
+        assert "spill stores" in out.stderr

@@ -32,6 +32,7 @@ def main():
     st = torch.empty((S, k + m, B), dtype=torch.uint8, device="cuda")
     rsp.synth_fill(st, k, seed=0)
     er = synth.erasure_table(a.config, 0, S)
+    plan.prepare(er)
     for _ in range(a.reps):
         plan.encode_batch(st)
         plan.decode_batch(st, er)
