@@ -351,7 +351,7 @@ static void decode_stripe(bulk_job *J, size_t s) {
   const orc_tables *T = J->T;
   int k = J->k, m = J->m, n = k + m, w = J->w;
   const int32_t *row = J->erasures + s * (size_t)m;
-  int er[ORC_MAXM], t = 0;
+  int er[ORC_MAXM] = {0}, t = 0;
   for (int i = 0; i < m; ++i)
     if (row[i] >= 0) er[t++] = row[i];
   if (check_erasures(n, m, er, t)) { J->rc = -3; return; }

@@ -25,6 +25,17 @@ __device__ __forceinline__ void stg_v4(void *p, uint4 v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
+// 256-bit accesses need PTX ISA 8.8 (CUDA 12.9); an older NVRTC gets RS_NO_V8 and two v4s.
+#ifdef RS_NO_V8
+__device__ __forceinline__ void ldg_v8(const void *p, uint32_t *r) {
+  const uint4 a = ldg_v4(p), b = ldg_v4(static_cast<const uint8_t *>(p) + 16);
+  r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+}
+__device__ __forceinline__ void stg_v8(void *p, const uint32_t *r) {
+  stg_v4(p, make_uint4(r[0], r[1], r[2], r[3]));
+  stg_v4(static_cast<uint8_t *>(p) + 16, make_uint4(r[4], r[5], r[6], r[7]));
+}
+#else
 __device__ __forceinline__ void ldg_v8(const void *p, uint32_t *r) {
   asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
@@ -36,6 +47,7 @@ __device__ __forceinline__ void stg_v8(void *p, const uint32_t *r) {
                   "r"(r[7])
                : "memory");
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // bit-plane transposes (delta swaps; each is an involution, so the same

@@ -13,6 +13,8 @@
 #include <array>
 #include <atomic>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -284,6 +286,11 @@ const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const MaskKey &key, const
       const std::string src = rsb::jit::source(*F, spec, &xors);
       auto k = std::make_shared<rsb::jit::Kernel>(rsb::jit::compile(src));
       k->xors = xors;
+      if (!k->ok) {  // loud, once per process (the pattern then runs on the table kernel)
+        static std::atomic<int> reported{0};
+        if (reported.fetch_add(1) == 0 || std::getenv("RS_POLY_JIT_LOG"))
+          std::fprintf(stderr, "[rs_poly] JIT compile/load failed (falling back to tables): %s\n", k->log.c_str());
+      }
       prom->set_value(k);
     };
     if (block) job();
