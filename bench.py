@@ -68,6 +68,15 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(cfg: str, op: str):
+    """DRAM bytes per call of the dominant kernel from the committed ncu capture (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return int(json.load(f)[cfg][op]["bytes_per_call"])
+    except Exception:
+        return None
+
+
 def allreduce(x: float, op: str, world: int, device) -> float:
     """Max/sum of a scalar over ranks (NCCL on the GPU box; gloo in tests/test_dist_gloo.py)."""
     if world == 1:
@@ -313,6 +322,7 @@ def run_ours(args):
     dec_kernel = "rs_jit (per-pattern NVRTC XOR network)" if jst["jit_launches"] else "sliced_kernel decode (tables)"
     dom_ms, dom_name = (dec_avg, "decode: " + dec_kernel) if dec_avg >= enc_avg else (enc_avg, "encode: sliced_kernel")
     achieved = moved / (dom_ms / 1e3) / 1e9
+    traffic = ncu_traffic(args.config, "decode" if dom_name.startswith("decode") else "encode")
 
     # ---- end to end through the public API from pinned host memory ----
     e2e = None
@@ -333,7 +343,7 @@ def run_ours(args):
                    "kernels": plan.kernel_kind,
                    "l2": f"inputs {S * n * B / 2**30:.1f} GiB per GPU >> 126 MB L2: no flush needed"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": f"{dom_name}; {moved} algorithmic bytes per call = S*(k+m)*B, avg {dom_ms:.4f} ms",
                      "peak_source": peak_src},
         "encode": {"gbs_user": round(user_bytes / (enc_avg / 1e3) / 1e9, 2), "ms": round(enc_avg, 4),
