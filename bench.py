@@ -386,11 +386,39 @@ def verify_encode_sampled(stripes, c) -> int:
     return bad
 
 
+def gpu_local_cpus(index: int):
+    """CPUs NVML reports as local to GPU `index` (its NUMA node), within our affinity; None if unknown."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, mk in enumerate(words) for b in range(64) if (mk >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
 def run_e2e(args, plan, stripes, er, c, world, dev, barrier):
     import torch
     K = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 5)
     K = max(1, K)
     S, k, B = c["stripes"], c["k"], c["block_bytes"]
+    # pinned buffers and the copy-issuing thread on the GPU's own NUMA node: pages are
+    # placed where they are first touched, and a remote node costs PCIe bandwidth
+    old_aff = os.sched_getaffinity(0)
+    local = gpu_local_cpus(dev.index if dev.index is not None else 0)
+    if local:
+        os.sched_setaffinity(0, local)
+    try:
+        return _run_e2e(K, plan, stripes, er, S, k, B, world, dev, barrier, local, len(old_aff))
+    finally:
+        os.sched_setaffinity(0, old_aff)
+
+
+def _run_e2e(K, plan, stripes, er, S, k, B, world, dev, barrier, local, n_all):
+    import torch
     host = torch.empty(tuple(stripes.shape), dtype=torch.uint8, pin_memory=True)
     host.copy_(stripes)
     plan.encode_host(host)  # warm
@@ -398,9 +426,14 @@ def run_e2e(args, plan, stripes, er, c, world, dev, barrier):
     barrier()
     t0 = time.perf_counter()
     h2d = d2h = 0
+    t_enc, t_dec = [], []
     for _ in range(K):
+        ta = time.perf_counter()
         a, b = plan.encode_host(host)
+        tb = time.perf_counter()
         c2, d = plan.decode_host(host, er)
+        t_enc.append(tb - ta)
+        t_dec.append(time.perf_counter() - tb)
         h2d += a + c2
         d2h += b + d
     barrier()
@@ -409,6 +442,9 @@ def run_e2e(args, plan, stripes, er, c, world, dev, barrier):
     value = step_throughput(S * k * B, 2, world, el / K * 1e3)
     return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K,
             "steps": K, "ms_per_step": round(el / K * 1e3, 3), "verified": bool(ok),
+            "encode_host_ms": round(statistics.median(t_enc) * 1e3, 2),
+            "decode_host_ms": round(statistics.median(t_dec) * 1e3, 2),
+            "host_cpus": (f"{len(local)} GPU-local CPUs of {n_all} (NVML affinity)" if local else "all"),
             "how": "rs_poly_encode_host + rs_poly_decode_host on pinned host stripes; host->device inputs, "
                    "device->host outputs inside the timed region (wall clock, max over ranks)"}
 

@@ -115,7 +115,9 @@ rs_status rs_poly_decode_batch(const rs_poly_plan *plan, void *stripes, size_t n
  * Same operations, but `host_stripes` is HOST memory (page-locked for full
  * speed, e.g. cudaHostAlloc / torch pin_memory), laid out as in the batched
  * calls.  The library streams chunks of stripes through device staging
- * buffers it allocates on `stream`'s device: host->device copy of the inputs
+ * buffers on `stream`'s device (3 lanes of ~256 MiB, kept by the plan for reuse
+ * and freed by rs_poly_plan_destroy; a call that finds them in use by another
+ * thread allocates its own for the call): host->device copy of the inputs
  * (encode: the k data blocks; decode: the n-t survivors), the kernel, and the
  * device->host copy of the outputs (encode: m parity blocks; decode: the t
  * erased blocks), overlapped across chunks.  Returns after the results are in

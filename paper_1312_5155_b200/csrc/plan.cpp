@@ -122,7 +122,42 @@ struct rs_poly_plan {
   mutable std::map<MaskKey, std::shared_ptr<JitEntry>> jit;
   mutable std::map<int, std::vector<cudaStream_t>> pool;  // device -> side streams for concurrent launches
   mutable std::atomic<uint64_t> jit_launches{0}, table_launches{0};
+  // pinned host slots for the per-call constant blob: a pageable cudaMemcpyAsync may
+  // wait for the stream, stalling the host between back-to-back calls
+  struct PinnedSlot {
+    uint8_t *p = nullptr;
+    size_t cap = 0;
+    int dev = 0;
+    cudaEvent_t ev = nullptr;
+    bool busy = false;
+  };
+  mutable std::mutex stage_mu;
+  mutable std::vector<PinnedSlot> stage;
+  // device staging of the host entry points (rs_poly_*_host), one per device, reused
+  // across calls: a fresh stream-ordered allocation per call would be re-mapped each
+  // time the default pool trims at the call's final synchronize
+  struct Staging {
+    std::mutex busy;
+    uint8_t *p = nullptr;
+    size_t cap = 0;
+  };
+  mutable std::map<int, std::unique_ptr<Staging>> staging;
   ~rs_poly_plan() {
+    for (auto &kv : staging)
+      if (kv.second->p) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(kv.first);
+        cudaFree(kv.second->p);
+        cudaSetDevice(cur);
+      }
+    for (auto &sl : stage) {
+      if (sl.ev) {
+        cudaEventSynchronize(sl.ev);
+        cudaEventDestroy(sl.ev);
+      }
+      if (sl.p) cudaFreeHost(sl.p);
+    }
     for (auto &kv : jit) {
       if (kv.second->fut.valid()) {
         auto k = kv.second->fut.get();
@@ -318,6 +353,28 @@ uint64_t body_units_of(const rs_poly_plan &P, const Geometry &G) {
   return G.aligned32 ? G.block_bytes / UB : 0;
 }
 
+int sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  int v = cache[dev].load();
+  if (!v) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev].store(v);
+  }
+  return v;
+}
+
+// Units (32 columns each) per CTA for a launch over `total` units: up to kSlicedUnitsPerCta,
+// fewer when that would leave less than ~8 CTAs per SM (single stripes, per-pattern launches).
+uint32_t units_per_cta_for(uint64_t total) {
+  const uint64_t target = (uint64_t)sm_count() * 8;
+  uint64_t upc = (total + target - 1) / target;
+  upc = (upc + kSlicedThreads - 1) / kSlicedThreads * kSlicedThreads;
+  return (uint32_t)std::min<uint64_t>(std::max<uint64_t>(upc, kSlicedThreads), kSlicedUnitsPerCta);
+}
+
 cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32_t *stripes, uint64_t n_sel,
                        uint64_t body_units, cudaStream_t st) {
   rsb::jit::Args a{};
@@ -329,8 +386,8 @@ cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32
   a.stripes = stripes;
   a.n_sel = n_sel;
   a.units_per_stripe = body_units;
-  a.units_per_cta = kSlicedUnitsPerCta;
-  a.ctas_per_stripe = (uint32_t)((body_units + kSlicedUnitsPerCta - 1) / kSlicedUnitsPerCta);
+  a.units_per_cta = units_per_cta_for(n_sel * body_units);
+  a.ctas_per_stripe = (uint32_t)((body_units + a.units_per_cta - 1) / a.units_per_cta);
   const uint64_t grid = n_sel * a.ctas_per_stripe;
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
@@ -347,8 +404,8 @@ cudaError_t launch_sliced_body(const rs_poly_plan &P, bool decode, const Geometr
   a.L = G.L;
   a.n_stripes = G.n_stripes;
   a.units_per_stripe = body_units;
-  a.units_per_cta = kSlicedUnitsPerCta;
-  a.ctas_per_stripe = (uint32_t)((body_units + kSlicedUnitsPerCta - 1) / kSlicedUnitsPerCta);
+  a.units_per_cta = units_per_cta_for(G.n_stripes * body_units);
+  a.ctas_per_stripe = (uint32_t)((body_units + a.units_per_cta - 1) / a.units_per_cta);
   if (decode) {
     a.pats = reinterpret_cast<const rsb::SlicedPat *>(dev + pats_off);
     a.pat_idx = reinterpret_cast<const int32_t *>(dev + idx_off);
@@ -380,14 +437,54 @@ cudaError_t launch_generic_range(const rs_poly_plan &P, const Geometry &G, uint6
   return rsb::launch_generic(P.w, a, st);
 }
 
+// Copy `bytes` at `src` to device `dst` on stream `s` through one of the plan's pinned
+// slots (reused once its previous copy has completed); pageable only if no slot can be had.
+cudaError_t upload_pinned(const rs_poly_plan &P, void *dst, const void *src, size_t bytes, cudaStream_t s) {
+  constexpr size_t kMaxSlots = 64;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  rs_poly_plan::PinnedSlot *slot = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(P.stage_mu);
+    for (auto &sl : P.stage)
+      if (!sl.busy && sl.dev == dev && sl.cap >= bytes && cudaEventQuery(sl.ev) == cudaSuccess) {
+        slot = &sl;
+        break;
+      }
+    if (!slot && P.stage.size() < kMaxSlots) {
+      rs_poly_plan::PinnedSlot sl;
+      sl.dev = dev;
+      sl.cap = std::max<size_t>(bytes, 64 << 10);
+      if (cudaHostAlloc(reinterpret_cast<void **>(&sl.p), sl.cap, cudaHostAllocDefault) == cudaSuccess &&
+          cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming) == cudaSuccess) {
+        P.stage.reserve(kMaxSlots);  // slots never move: pointers into the vector stay valid
+        P.stage.push_back(sl);
+        slot = &P.stage.back();
+      } else {
+        if (sl.p) cudaFreeHost(sl.p);
+        cudaGetLastError();
+      }
+    }
+    if (slot) slot->busy = true;
+  }
+  if (!slot) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  std::memcpy(slot->p, src, bytes);
+  cudaError_t e = cudaMemcpyAsync(dst, slot->p, bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaEventRecord(slot->ev, s);
+  if (e != cudaSuccess) cudaStreamSynchronize(s);  // never hand out a slot a copy may still read
+  std::lock_guard<std::mutex> lock(P.stage_mu);
+  slot->busy = false;
+  return e;
+}
+
 struct DevBlob {
   uint8_t *p = nullptr;
   cudaStream_t st = nullptr;
-  cudaError_t upload(const Blob &b, cudaStream_t s) {
+  cudaError_t upload(const rs_poly_plan &P, const Blob &b, cudaStream_t s) {
     st = s;
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p), std::max<size_t>(b.h.size(), 16), s);
     if (e != cudaSuccess) return e;
-    return cudaMemcpyAsync(p, b.h.data(), b.h.size(), cudaMemcpyHostToDevice, s);
+    return upload_pinned(P, p, b.h.data(), b.h.size(), s);
   }
   cudaError_t release() {
     cudaError_t e = p ? cudaFreeAsync(p, st) : cudaSuccess;
@@ -420,7 +517,7 @@ rs_status encode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs, c
   const size_t pats_off = b.add(&gp, sizeof(gp));
   const size_t tables_off = b.add(P->enc_tab.data(), P->enc_tab.size());
   DevBlob d;
-  cudaError_t e = d.upload(b, st);
+  cudaError_t e = d.upload(*P, b, st);
   if (e == cudaSuccess && ptrs) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
   if (e == cudaSuccess && body) {
     if (P->sliced) {
@@ -539,7 +636,7 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   const uint32_t smem = max_in * (P->w == 8 ? 128 : 512);
 
   DevBlob d;
-  cudaError_t e = d.upload(b, st);
+  cudaError_t e = d.upload(*P, b, st);
   if (e == cudaSuccess && ptrs) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
   // table-driven body for stripes without a ready JIT kernel
   if (e == cudaSuccess && body && any_rt) {
@@ -883,13 +980,34 @@ rs_status host_impl(const rs_poly_plan *P, bool decode, uint8_t *host, size_t n_
   const uint64_t per_chunk = std::max<uint64_t>(1, kStagingTarget / stripe_dev);
   cudaStream_t lanes[kNumLanes] = {};
   uint8_t *stage[kNumLanes] = {};
+  bool owned_async = false;  // staging from cudaMallocAsync (plan staging busy in another call)
   cudaEvent_t start = nullptr;
   cudaError_t e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventRecord(start, user);
+  const size_t lane_bytes = per_chunk * stripe_dev;
+  rs_poly_plan::Staging *sg = nullptr;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(P->mu);
+    auto &slot = P->staging[dev];
+    if (!slot) slot = std::make_unique<rs_poly_plan::Staging>();
+    if (slot->busy.try_lock()) sg = slot.get();
+  }
+  if (sg && e == cudaSuccess && sg->cap < lane_bytes * kNumLanes) {
+    if (sg->p) cudaFree(sg->p);  // idle: its last user synchronized before releasing it
+    sg->p = nullptr;
+    sg->cap = 0;
+    e = cudaMalloc(reinterpret_cast<void **>(&sg->p), lane_bytes * kNumLanes);
+    if (e == cudaSuccess) sg->cap = lane_bytes * kNumLanes;
+  }
+  owned_async = sg == nullptr;
   for (int l = 0; l < kNumLanes && e == cudaSuccess; ++l) {
     e = cudaStreamCreateWithFlags(&lanes[l], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(lanes[l], start, 0);
-    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void **>(&stage[l]), per_chunk * stripe_dev, lanes[l]);
+    if (e != cudaSuccess) break;
+    if (owned_async) e = cudaMallocAsync(reinterpret_cast<void **>(&stage[l]), lane_bytes, lanes[l]);
+    else stage[l] = sg->p + (size_t)l * lane_bytes;
   }
   rc = cuda_status(e);
   for (size_t s0 = 0, ci = 0; rc == RS_OK && s0 < n_stripes; s0 += per_chunk, ++ci) {
@@ -940,13 +1058,14 @@ rs_status host_impl(const rs_poly_plan *P, bool decode, uint8_t *host, size_t n_
     if (e != cudaSuccess) rc = cuda_status(e);
   }
   for (int l = 0; l < kNumLanes; ++l) {
-    if (stage[l]) cudaFreeAsync(stage[l], lanes[l]);
+    if (stage[l] && owned_async) cudaFreeAsync(stage[l], lanes[l]);
     if (lanes[l]) {
       cudaError_t es = cudaStreamSynchronize(lanes[l]);
       if (rc == RS_OK && es != cudaSuccess) rc = cuda_status(es);
       cudaStreamDestroy(lanes[l]);
     }
   }
+  if (sg) sg->busy.unlock();
   if (start) cudaEventDestroy(start);
   if (h2d) *h2d = in_bytes;
   if (d2h) *d2h = out_bytes;
