@@ -124,6 +124,48 @@ __device__ __forceinline__ void transposeW(uint32_t *x) {
   else transpose16(x);
 }
 
+// ---------------------------------------------------------------------------
+// Horner steps on bit-planes (syndrome form): S <- S * alpha^J (+ c).
+// Multiplication by the constant alpha^J is GF(2)-linear: plane o of the product is
+// the XOR of the planes b with bit o of alpha^J * 2^b set.  The matrix is evaluated
+// at compile time from (W, POLY); after unrolling only the XORs remain (alpha^J is
+// sparse for small J: 3 extra XORs per power for 0x11D and 0x1100B).
+// ---------------------------------------------------------------------------
+template <int W, uint32_t POLY>
+struct GFc {
+  __host__ __device__ static constexpr uint32_t mul(uint32_t a, uint32_t b) {
+    uint32_t r = 0;
+    for (int i = 0; i < W; ++i) {
+      if ((b >> i) & 1u) r ^= a;
+      a <<= 1;
+      if ((a >> W) & 1u) a ^= POLY;
+    }
+    return r;
+  }
+  __host__ __device__ static constexpr uint32_t alpha_pow(int e) {
+    uint32_t r = 1;
+    for (int i = 0; i < e; ++i) r = mul(r, 2u);
+    return r;
+  }
+  // bit o of alpha^J * 2^b
+  __host__ __device__ static constexpr bool bit(int J, int b, int o) { return (mul(alpha_pow(J), 1u << b) >> o) & 1u; }
+};
+
+template <int W, uint32_t POLY, int J, bool ADD>
+__device__ __forceinline__ void horner_step(uint32_t *s, const uint32_t *c) {
+  uint32_t o[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) o[i] = s[i];
+#pragma unroll
+  for (int ob = 0; ob < W; ++ob) {
+    uint32_t acc = ADD ? c[ob] : 0u;
+#pragma unroll
+    for (int b = 0; b < W; ++b)
+      if (GFc<W, POLY>::bit(J, b, ob)) acc ^= o[b];
+    s[ob] = acc;
+  }
+}
+
 template <int W>
 __device__ __forceinline__ void load_unit(const uint8_t *p, uint32_t *x) {
   ldg_v8(p, x);

@@ -39,8 +39,14 @@ INSTANCES = [
     (12, 4, 8, 0x11D, 12),
     (8, 4, 8, 0x11D, 8),
     (6, 4, 8, 0x11D, 6),
-    (12, 4, 16, 0x1100B, 3),  # config C4 (groups keep the 192 input planes out of registers)
+    (12, 4, 16, 0x1100B, 0),  # config C4: syndrome-form (Horner + Q) encoder, see emit_horner
 ]
+# w = 16 instances use the syndrome form of the encoder (P:237-241 with the symmetric use of
+# P:306): H_j = Horner over the data planes with step alpha^j (sparse, compile-time in
+# bitslice_device.cuh), then parity = Q H with Q = Vp^{-1} diag(alpha^{jm}) emitted here.
+# A direct 64 x 192 parity-map network needs ~2400 XORs in register-sized CSE groups;
+# Horner (~715 LOP3) + Q (~620 XORs) streams one block at a time.
+HORNER_W = (16,)
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "rs_networks.cuh")
 
@@ -124,7 +130,81 @@ def paar(R: np.ndarray):
     return temps, rows
 
 
+def gf_pow(a: int, e: int, w: int, poly: int) -> int:
+    r = 1
+    for _ in range(e):
+        r = gf_mul(r, a, w, poly)
+    return r
+
+
+def gf_inv_matrix(A: list[list[int]], w: int, poly: int) -> list[list[int]]:
+    t = len(A)
+    M = [list(row) + [1 if r == c else 0 for c in range(t)] for r, row in enumerate(A)]
+    for c in range(t):
+        p = next(r for r in range(c, t) if M[r][c])
+        M[c], M[p] = M[p], M[c]
+        iv = gf_pow(M[c][c], (1 << w) - 2, w, poly)
+        M[c] = [gf_mul(iv, v, w, poly) for v in M[c]]
+        for r in range(t):
+            if r != c and M[r][c]:
+                f = M[r][c]
+                M[r] = [v ^ gf_mul(f, u, w, poly) for v, u in zip(M[r], M[c])]
+    return [row[t:] for row in M]
+
+
+def horner_q(k: int, m: int, w: int, poly: int) -> list[list[int]]:
+    """Q (m x m): parity p = Q H, H_j = sum_b d_b alpha^{j b} (Horner over the data).
+
+    Every codeword has zero syndromes at alpha^0..alpha^{m-1} (roots of g), so
+    sum_i p_i alpha^{j i} = S_j(data) = alpha^{j m} H_j (char 2); p = Vp^{-1} diag(alpha^{jm}) H."""
+    a = 2
+    Vp = [[gf_pow(gf_pow(a, i, w, poly), j, w, poly) for i in range(m)] for j in range(m)]
+    Vi = gf_inv_matrix(Vp, w, poly)
+    return [[gf_mul(Vi[i][j], gf_pow(a, j * m, w, poly), w, poly) for j in range(m)] for i in range(m)]
+
+
+def gf_bit_matrix(M: list[list[int]], w: int, poly: int) -> np.ndarray:
+    rows, cols = len(M), len(M[0])
+    R = np.zeros((rows * w, cols * w), dtype=bool)
+    for i in range(rows):
+        for j in range(cols):
+            for b in range(w):
+                prod = gf_mul(M[i][j], 1 << b, w, poly)
+                for o in range(w):
+                    if (prod >> o) & 1:
+                        R[i * w + o, j * w + b] = True
+    return R
+
+
+def emit_horner(k: int, m: int, w: int, poly: int) -> str:
+    R = gf_bit_matrix(horner_q(k, m, w, poly), w, poly)
+    temps, rows = paar(R)
+    nin = m * w
+
+    def name(v: int) -> str:
+        return f"h[{v}]" if v < nin else f"t{v - nin}"
+
+    xors = len(temps) + sum(max(0, len(r) - 1) for r in rows)
+    out = [
+        f"// RS({k},{m}) over GF(2^{w}) / 0x{poly:X}: syndrome-form encoder.  Q = Vp^-1 diag(alpha^jm),",
+        f"// bit-matrix {m * w}x{m * w} with {int(R.sum())} ones -> {xors} two-input XORs after CSE.",
+        f"template <> struct RsQNet<{k}, {m}, {w}, 0x{poly:X}u> {{",
+        f"  static constexpr bool kHorner = true;",
+        f"  static constexpr int kXors = {xors};",
+        f"  static __device__ __forceinline__ void run(const uint32_t (&h)[{nin}], uint32_t (&y)[{m * w}]) {{",
+    ]
+    for t, (a, b) in enumerate(temps):
+        out.append(f"    const uint32_t t{t} = {name(a)} ^ {name(b)};")
+    for r, terms in enumerate(rows):
+        expr = " ^ ".join(name(v) for v in terms) if terms else "0u"
+        out.append(f"    y[{r}] = {expr};")
+    out += ["  }", "};", ""]
+    return "\n".join(out)
+
+
 def emit_instance(k: int, m: int, w: int, poly: int, gsize: int) -> str:
+    if w in HORNER_W:
+        return emit_horner(k, m, w, poly)
     R = bit_matrix(k, m, w, poly)
     ngroups = (k + gsize - 1) // gsize
     total_xors = 0
@@ -183,6 +263,8 @@ def generate(out: str = OUT, force: bool = False) -> bool:
         "",
         "template <int K, int M, int W, uint32_t POLY> struct RsNet;  // only the instances below exist",
         "template <int K, int M, int W, uint32_t POLY, int G> struct RsNetGroup;",
+        "// syndrome-form encoders (w = 16): kHorner = true and run() = the Q network",
+        "template <int K, int M, int W, uint32_t POLY> struct RsQNet { static constexpr bool kHorner = false; };",
         "",
         "#define RS_NET_INSTANCES(X) \\",
     ]

@@ -104,6 +104,21 @@ inline bool invert(const Field &F, std::vector<uint32_t> &A, int t) {
   return true;
 }
 
+// Syndrome-form encoder matrix Q (m x m, row-major): parity p = Q H where
+// H_j = sum_b d_b alpha^{j b} (Horner over the data).  Every codeword has zero
+// syndromes at the roots alpha^0..alpha^{m-1} of g, so
+// sum_i p_i alpha^{j i} = alpha^{j m} H_j and Q = Vp^{-1} diag(alpha^{j m}),
+// Vp[j][i] = alpha^{j i} -- the decoder used to encode.
+inline std::vector<uint32_t> horner_q(const Field &F, int m) {
+  std::vector<uint32_t> V((size_t)m * m);
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < m; ++i) V[(size_t)j * m + i] = F.alpha_pow((uint64_t)j * (uint64_t)i);
+  if (!invert(F, V, m)) return {};
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) V[(size_t)i * m + j] = F.mul(V[(size_t)i * m + j], F.alpha_pow((uint64_t)j * m));
+  return V;
+}
+
 // Polynomial position of API block b (data b -> x^{m+b}, parity b -> x^{b-k}).
 inline int position(int b, int k, int m) { return b < k ? m + b : b - k; }
 

@@ -25,6 +25,18 @@ struct Spec {
   std::vector<uint32_t> M;   // out x in GF(2^w) matrix, row-major
   int group_blocks = 0;      // inputs per CSE group (0 = all)
   int min_blocks = 4;        // __launch_bounds__ min CTAs/SM
+  // Syndrome (Horner) form, used for w = 16: `seq` lists the API block at
+  // each polynomial position from the highest down (-1 = erased: multiply only), T
+  // syndromes S_j = sum_p c_p alpha^{j p'} are folded with step alpha^j, and the
+  // outputs are M (out x T) applied to S.  in_blk is unused in this form.
+  bool horner = false;
+  uint32_t poly = 0;
+  std::vector<int> seq;
+  int T = 0;
+  // loop_positions: emit the positions after the first survivor as a runtime loop
+  // (seq[i] is at position pos_top - i; block of a position: data pos-m, parity k+pos)
+  bool loop_positions = false;
+  int pos_top = 0, k = 0, m = 0;
 };
 
 struct Kernel {

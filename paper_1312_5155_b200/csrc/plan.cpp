@@ -39,6 +39,7 @@ struct PatternHost {
   std::vector<int> erased;  // row order of W / R: ascending API index
   std::vector<int> surv;    // survivors, ascending API index (columns of R)
   std::vector<uint32_t> R;  // t x (n-t) decode matrix V_E^{-1} A_E
+  std::vector<uint32_t> Vinv;  // t x t, V_E^{-1} (Step 2)
   rsb::SlicedPat sp{};
   std::vector<uint8_t> wtab;  // sliced W tables
   rsb::GenericPat gp{};
@@ -208,6 +209,7 @@ std::shared_ptr<const PatternHost> build_pattern(const rs_poly_plan &P, const st
   for (int j = 0; j < t; ++j)
     for (int e = 0; e < t; ++e) V[(size_t)j * t + e] = F.alpha_pow((uint64_t)F.log_[X[e]] * (uint64_t)j);
   if (!rsb::invert(F, V, t)) return nullptr;  // Opt3: V^{-1} once per pattern
+  ph->Vinv = V;
   // W = V^{-1} H_par[0:t, :]  (t x m)
   std::vector<uint32_t> W((size_t)t * m, 0);
   for (int e = 0; e < t; ++e)
@@ -292,6 +294,60 @@ rsb::jit::Spec jit_spec(const rs_poly_plan &P, const std::vector<int> &in, const
   return s;
 }
 
+// Syndrome-form JIT kernels are fully unrolled (compile-time erased set; loads of all
+// positions in flight).  RS_POLY_JIT_LOOP=1 emits a compact position loop instead
+// (measured slower on C4: 9.2 vs 6.6 ms -- one block in flight per thread).
+bool jit_loop_positions() {
+  static const bool v = std::getenv("RS_POLY_JIT_LOOP") && std::getenv("RS_POLY_JIT_LOOP")[0] == '1';
+  return v;
+}
+
+// The encoder kernel of a code without a compiled network: w = 8 the parity-map
+// network, w = 16 the syndrome form (Horner over the data, then Q).
+rsb::jit::Spec encoder_spec(const rs_poly_plan &P) {
+  std::vector<int> in(P.k), out(P.m);
+  for (int j = 0; j < P.k; ++j) in[j] = j;
+  for (int i = 0; i < P.m; ++i) out[i] = P.k + i;
+  rsb::jit::Spec s = jit_spec(P, in, out, P.pmap);
+  if (P.w == 16) {
+    s.horner = true;
+    s.poly = P.poly;
+    s.T = P.m;
+    s.M = rsb::horner_q(P.F, P.m);
+    for (int j = P.k - 1; j >= 0; --j) s.seq.push_back(j);  // positions m+k-1 .. m
+    s.min_blocks = 3;
+    s.loop_positions = jit_loop_positions();
+    s.pos_top = P.m + P.k - 1;
+    s.k = P.k;
+    s.m = P.m;
+  }
+  return s;
+}
+
+// The decoder kernel of one erasure pattern: w = 8 the network of R = V_E^{-1} A_E over
+// the survivors; w = 16 Horner over all n positions (erased: multiply only), then V_E^{-1}.
+rsb::jit::Spec decoder_spec(const rs_poly_plan &P, const PatternHost &ph) {
+  rsb::jit::Spec s = jit_spec(P, ph.surv, ph.erased, ph.R);
+  if (P.w == 16) {
+    s.horner = true;
+    s.poly = P.poly;
+    s.T = (int)ph.erased.size();
+    s.M = ph.Vinv;
+    std::vector<char> er(P.n, 0);
+    for (int b : ph.erased) er[b] = 1;
+    for (int pos = P.n - 1; pos >= 0; --pos) {
+      const int b = pos >= P.m ? pos - P.m : P.k + pos;  // inverse of rsb::position
+      s.seq.push_back(er[b] ? -1 : b);
+    }
+    s.min_blocks = 3;
+    s.loop_positions = jit_loop_positions();
+    s.pos_top = P.n - 1;
+    s.k = P.k;
+    s.m = P.m;
+  }
+  return s;
+}
+
 // The compiled kernel for `key` if it is ready; schedules (background) or runs (sync /
 // wait) its compilation on first request.  Must be called without holding P.mu.
 const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const MaskKey &key, const std::function<rsb::jit::Spec()> &mk,
@@ -340,7 +396,12 @@ std::vector<cudaStream_t> side_streams(const rs_poly_plan &P) {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(P.mu);
   auto &v = P.pool[dev];
-  while (v.size() < 3) {
+  static const size_t want = [] {
+    const char *e = std::getenv("RS_POLY_SIDE_STREAMS");  // tuning knob; default 0 (PDL chain)
+    const long v = e ? std::strtol(e, nullptr, 10) : 0;
+    return (size_t)std::max(0L, std::min(v, 63L));
+  }();
+  while (v.size() < want) {
     cudaStream_t s = nullptr;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) break;
     v.push_back(s);
@@ -376,7 +437,7 @@ uint32_t units_per_cta_for(uint64_t total) {
 }
 
 cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32_t *stripes, uint64_t n_sel,
-                       uint64_t body_units, cudaStream_t st) {
+                       uint64_t body_units, cudaStream_t st, bool pdl = false) {
   rsb::jit::Args a{};
   a.base = G.L.base;
   a.stripe_stride = G.L.stripe_stride;
@@ -393,8 +454,21 @@ cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32
   if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
   void *args[] = {&a};
   rsb::count_launch();
-  return cudaLaunchKernel(reinterpret_cast<const void *>(k.fn), dim3((unsigned)grid), dim3(kSlicedThreads), args, 0,
-                          st);
+  if (!pdl)
+    return cudaLaunchKernel(reinterpret_cast<const void *>(k.fn), dim3((unsigned)grid), dim3(kSlicedThreads), args,
+                            0, st);
+  // programmatic dependent launch (the generated kernels trigger at entry and wait at exit)
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kSlicedThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(k.fn), args);
 }
 
 cudaError_t launch_sliced_body(const rs_poly_plan &P, bool decode, const Geometry &G, uint64_t body_units,
@@ -506,7 +580,7 @@ rs_status encode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs, c
     std::vector<int> in(P->k), out(P->m);
     for (int j = 0; j < P->k; ++j) in[j] = j;
     for (int i = 0; i < P->m; ++i) out[i] = P->k + i;
-    jk = jit_get(*P, kEncodeKey, [&] { return jit_spec(*P, in, out, P->pmap); }, false);
+    jk = jit_get(*P, kEncodeKey, [&] { return encoder_spec(*P); }, false);
   }
   if (!P->sliced && !jk) body = 0;
   Blob b;
@@ -571,7 +645,7 @@ rs_status collect_patterns(const rs_poly_plan *P, const std::vector<std::vector<
 
 const rsb::jit::Kernel *pattern_jit(const rs_poly_plan &P, const PatternHost &ph, const MaskKey &key, bool wait) {
   if (!jit_eligible(P, (int)ph.erased.size())) return nullptr;
-  return jit_get(P, key, [&] { return jit_spec(P, ph.surv, ph.erased, ph.R); }, wait);
+  return jit_get(P, key, [&] { return decoder_spec(P, ph); }, wait);
 }
 
 // rows: per stripe list of erased API indices (validated, sorted ascending)
@@ -649,8 +723,21 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   if (e == cudaSuccess)
     e = launch_generic_range(*P, G, body * UB, G.block_bytes, d.p, generic_pats_off, idx_off, tables_off,
                              max_groups, smem, st);
-  // JIT kernels, one launch per pattern, spread over side streams so short launches overlap
-  if (e == cudaSuccess && any_jit) {
+  // JIT kernels, one launch per pattern.  Default: one chain on the caller's stream with
+  // programmatic dependent launch, so each kernel's last wave overlaps the next kernel's
+  // first (a C4 stripe is only ~2.3 waves).  The first kernel of the chain is launched
+  // without the attribute: it must not overlap the work queued before this call.
+  // RS_POLY_SIDE_STREAMS=N > 0 instead spreads the launches over N extra streams.
+  if (e == cudaSuccess && any_jit && side_streams(*P).empty()) {
+    bool first = true;
+    for (size_t i = 0; i < pats.size() && e == cudaSuccess; ++i) {
+      if (groups[i].empty()) continue;
+      e = launch_jit(*jk[i], G, reinterpret_cast<const int32_t *>(d.p + grp_off[i]), groups[i].size(), body, st,
+                     !first);
+      first = false;
+      P->jit_launches++;
+    }
+  } else if (e == cudaSuccess && any_jit) {
     std::vector<cudaStream_t> side = side_streams(*P);
     cudaEvent_t fork = nullptr;
     e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
@@ -800,7 +887,7 @@ rs_status rs_poly_prepare(const rs_poly_plan *P, const int32_t *erasures, size_t
     std::vector<int> in(P->k), out(P->m);
     for (int j = 0; j < P->k; ++j) in[j] = j;
     for (int i = 0; i < P->m; ++i) out[i] = P->k + i;
-    jit_get(*P, kEncodeKey, [&] { return jit_spec(*P, in, out, P->pmap); }, false);
+    jit_get(*P, kEncodeKey, [&] { return encoder_spec(*P); }, false);
   }
   for (size_t i = 0; i < pats.size(); ++i) pattern_jit(*P, *pats[i], keys[i], false);  // queue all first
   std::vector<std::shared_ptr<JitEntry>> wait;
@@ -821,14 +908,14 @@ size_t rs_poly_jit_source(const rs_poly_plan *P, const int *erasures, int n_eras
     std::vector<int> in(P->k), out(P->m);
     for (int j = 0; j < P->k; ++j) in[j] = j;
     for (int i = 0; i < P->m; ++i) out[i] = P->k + i;
-    spec = jit_spec(*P, in, out, P->pmap);
+    spec = encoder_spec(*P);
   } else {
     std::vector<int32_t> row(erasures, erasures + n_erasures);
     std::vector<int> er;
     if (parse_row(P, row.data(), n_erasures, er, false) || !jit_eligible(*P, (int)er.size())) return 0;
     auto ph = build_pattern(*P, er);
     if (!ph) return 0;
-    spec = jit_spec(*P, ph->surv, ph->erased, ph->R);
+    spec = decoder_spec(*P, *ph);
   }
   const std::string s = rsb::jit::source(P->F, spec, nullptr);
   if (buf && cap) {

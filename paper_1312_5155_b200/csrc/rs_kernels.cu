@@ -56,6 +56,48 @@ __device__ __forceinline__ void net_groups(uint8_t *const *blk, uint64_t off, ui
     net_groups<K, M, W, POLY, DECODE, G + 1>(blk, off, emask, y);
 }
 
+// Syndrome-form encoder (w = 16 instances, RsQNet): H_j = Horner over the data
+// blocks from the highest position x^{m+k-1} down to x^m with step alpha^j
+// (P:237-241), one block in registers at a time, then y = Q H (Q = Vp^{-1}
+// diag(alpha^{jm}), the symmetric use of the decoder).  Erased data blocks
+// (decode) are not read: their planes are zero.
+template <int K, int M, int W, uint32_t POLY, bool DECODE, int J>
+__device__ __forceinline__ void horner_all(uint32_t (&h)[M * W], const uint32_t (&c)[W]) {
+  horner_step<W, POLY, J, true>(&h[J * W], c);
+  if constexpr (J + 1 < M) horner_all<K, M, W, POLY, DECODE, J + 1>(h, c);
+}
+
+template <int K, int M, int W, uint32_t POLY, bool DECODE>
+__device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off, uint32_t emask,
+                                              uint32_t (&y)[M * W]) {
+  uint32_t h[M * W];
+#pragma unroll
+  for (int jb = K - 1; jb >= 0; --jb) {
+    uint32_t c[W];
+    if (DECODE && ((emask >> jb) & 1u)) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) c[q] = 0;
+    } else {
+      load_unit<W>(blk[jb] + off, c);
+      transposeW<W>(c);
+    }
+    if (jb == K - 1) {
+#pragma unroll
+      for (int i = 0; i < M * W; ++i) h[i] = c[i % W];
+    } else {
+      horner_all<K, M, W, POLY, DECODE, 0>(h, c);
+    }
+  }
+  RsQNet<K, M, W, POLY>::run(h, y);
+}
+
+template <int K, int M, int W, uint32_t POLY, bool DECODE>
+__device__ __forceinline__ void encode_planes(uint8_t *const *blk, uint64_t off, uint32_t emask,
+                                              uint32_t (&y)[M * W]) {
+  if constexpr (RsQNet<K, M, W, POLY>::kHorner) horner_encode<K, M, W, POLY, DECODE>(blk, off, emask, y);
+  else net_groups<K, M, W, POLY, DECODE, 0>(blk, off, emask, y);
+}
+
 // ---------------------------------------------------------------------------
 // bit-sliced kernel
 // ---------------------------------------------------------------------------
@@ -63,8 +105,11 @@ __device__ __forceinline__ void net_groups(uint8_t *const *blk, uint64_t off, ui
 // occupancy matters more than registers.  Measured on B200 (profiles/r01b_occupancy_sweep.log):
 // w8 at 4 CTAs/SM (<=128 regs, a few spilled bytes) reaches the copy roofline on RS(10,4)
 // encode; w16 spills at 4 and runs best at 3.
+#ifndef RS_W16_MINB
+#define RS_W16_MINB 3
+#endif
 template <int W>
-constexpr int sliced_min_blocks() { return W == 8 ? 4 : 3; }
+constexpr int sliced_min_blocks() { return W == 8 ? 4 : RS_W16_MINB; }
 
 template <int K, int M, int W, uint32_t POLY, bool DECODE>
 __global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(const SlicedArgs a) {
@@ -101,7 +146,7 @@ __global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(con
   for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
     const uint64_t off = u * UB;
     uint32_t y[M * W];
-    net_groups<K, M, W, POLY, DECODE, 0>(blk, off, emask, y);
+    encode_planes<K, M, W, POLY, DECODE>(blk, off, emask, y);
 #pragma unroll
     for (int i = 0; i < M; ++i) transposeW<W>(&y[i * W]);
 

@@ -38,8 +38,106 @@ def parse(src):
     return w, ins, outs, groups, stores
 
 
+def evaluate_horner(src, cw_cols):
+    """Syndrome-form sources (w = 16): statements run in order on bit-planes; a
+    horner_step<W, POLY, J, ADD>(S_j, x) is executed by its contract -- every column
+    of S_j multiplied by alpha^J (tests/gfref.py's multiply, not the library's), plus
+    x if ADD -- so the generated Horner sequence and output network are checked."""
+    from tests import gfref
+    ins = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bi(\d+) = blkp\(a, s, (\d+)\);", src)}
+    outs = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bo(\d+) = blkp\(a, s, (\d+)\);", src)}
+    w = int(re.search(r"const uint64_t off = u \* (\d+)ull;", src).group(1)) * 8 // 32
+    body = src[src.index("const uint64_t off = u *"):]
+    C = cw_cols.shape[1]
+    S, x, y, env, res = {}, {}, {}, {}, {}
+
+    def planes(blk):
+        return [sum(((int(cw_cols[blk][c]) >> b) & 1) << c for c in range(C)) for b in range(w)]
+
+    def val(tok):
+        tok = tok.strip()
+        if tok == "0u":
+            return 0
+        mm = re.fullmatch(r"S\[(\d+)\]", tok)
+        return S[int(mm.group(1))] if mm else env[tok]
+
+    lines = [ln.strip() for ln in body.splitlines()]
+    # compact form: "for (int i = A; i < B; ++i) { if ((MASK >> i) & 1) {erased} else {survivor} }"
+    # is expanded here into straight-line statements with the block index substituted
+    out_lines, i = [], 0
+    while i < len(lines):
+        mm = re.fullmatch(r"for \(int i = (\d+); i < (\d+); \+\+i\) \{", lines[i])
+        if not mm:
+            out_lines.append(lines[i])
+            i += 1
+            continue
+        lo, hi = int(mm.group(1)), int(mm.group(2))
+        emask = int(re.fullmatch(r"if \(\((\d+)ull >> i\) & 1ull\) \{", lines[i + 1]).group(1))
+        j = i + 2
+        er_body = []
+        while lines[j] != "} else {":
+            er_body.append(lines[j])
+            j += 1
+        j += 1
+        sv_body = []
+        while lines[j] != "}":
+            sv_body.append(lines[j])
+            j += 1
+        assert lines[j + 1] == "}"
+        pos_top = int(re.fullmatch(r"const int pos = (\d+) - i;", sv_body[0]).group(1))
+        mb = re.fullmatch(r"const int b = pos >= (\d+) \? pos - (\d+) : (\d+) \+ pos;", sv_body[1])
+        M_, K_ = int(mb.group(1)), int(mb.group(3))
+        for it in range(lo, hi):
+            if (emask >> it) & 1:
+                out_lines += er_body
+            else:
+                pos = pos_top - it
+                blk = pos - M_ if pos >= M_ else K_ + pos
+                for ln in sv_body[2:]:
+                    out_lines.append(ln.replace("blkp(a, s, b)", f"blkp(a, s, {blk})"))
+        i = j + 2
+    for line in out_lines:
+        if mm := re.fullmatch(r"load_unit<\d+>\(blkp\(a, s, (\d+)\) \+ off, x\);", line):
+            x = dict(enumerate(planes(int(mm.group(1)))))
+            continue
+        if mm := re.fullmatch(r"uint32_t S\[(\d+)\];", line):
+            S = {q: 0 for q in range(int(mm.group(1)))}
+        elif mm := re.fullmatch(r"load_unit<\d+>\(bi(\d+) \+ off, x\);", line):
+            x = dict(enumerate(planes(ins[int(mm.group(1))])))
+        elif mm := re.fullmatch(r"for \(int q = 0; q < (\d+); \+\+q\) S\[q\] = x\[q % (\d+)\];", line):
+            for q in range(int(mm.group(1))):
+                S[q] = x[q % int(mm.group(2))]
+        elif mm := re.fullmatch(r"for \(int q = 0; q < (\d+); \+\+q\) S\[q\] = 0u;", line):
+            for q in range(int(mm.group(1))):
+                S[q] = 0
+        elif mm := re.fullmatch(r"horner_step<(\d+), (\d+)u, (\d+), (true|false)>\(&S\[(\d+)\], (x|nullptr)\);", line):
+            W, poly, J, add, base = int(mm.group(1)), int(mm.group(2)), int(mm.group(3)), mm.group(4), int(mm.group(5))
+            aj = 1
+            for _ in range(J):
+                aj = gfref.mul(aj, 2, poly)
+            syms = [sum(((S[base + b] >> c) & 1) << b for b in range(W)) for c in range(C)]
+            syms = [gfref.mul(v, aj, poly) for v in syms]
+            if add == "true":
+                syms = [v ^ sum(((x[b] >> c) & 1) << b for b in range(W)) for c, v in enumerate(syms)]
+            for b in range(W):
+                S[base + b] = sum(((syms[c] >> b) & 1) << c for c in range(C))
+        elif mm := re.fullmatch(r"const uint32_t (t\d+) = (.*);", line):
+            env[mm.group(1)] = val(mm.group(2).split("^")[0]) ^ val(mm.group(2).split("^")[1])
+        elif mm := re.fullmatch(r"y\[(\d+)\] = (.*);", line):
+            v = 0
+            for tok in mm.group(2).split("^"):
+                v ^= val(tok)
+            y[int(mm.group(1))] = v
+        elif mm := re.fullmatch(r"store_unit<\d+>\(bo(\d+) \+ off, &y\[(\d+)\]\);", line):
+            i, base = int(mm.group(1)), int(mm.group(2))
+            res[outs[i]] = [sum(((y[base + o] >> c) & 1) << o for o in range(w)) for c in range(C)]
+    return res
+
+
 def evaluate(src, cw_cols):
     """cw_cols: [n][C] symbols (API order).  Returns {out_block: [C] symbols}."""
+    if "horner_step<" in src:
+        return evaluate_horner(src, cw_cols)
     w, ins, outs, groups, stores = parse(src)
     C = cw_cols.shape[1]
     nout = len(outs)
