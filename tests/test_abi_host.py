@@ -165,10 +165,57 @@ def eval_network(groups, data_planes, m, w):
     return y
 
 
+def horner_parity(k, m, w, poly, data):
+    """Syndrome-form instances (RsQNet): H_j = sum_b d_b alpha^{j b} computed here with
+    tests/gfref.py (the Horner steps' contract), then the generated Q network."""
+    from tests import gfref
+    src = open(os.path.join(PKG, "csrc", "rs_networks.cuh")).read()
+    mt = re.search(r"template <> struct RsQNet<%d, %d, %d, 0x%Xu> \{(.*?)\n\};" % (k, m, w, poly), src, re.S)
+    assert mt, "instance not found"
+    stmts = re.findall(r"^\s+(?:const uint32_t (t\d+)|y\[(\d+)\]) = (.*);$", mt.group(1), re.M)
+    cols = data.shape[1]
+    H = []
+    for j in range(m):
+        aj = 1
+        for _ in range(j):
+            aj = gfref.mul(aj, 2, poly)
+        row = []
+        for c in range(cols):
+            acc = 0
+            for b in range(k - 1, -1, -1):      # Horner from the highest data position down
+                acc = gfref.mul(acc, aj, poly) ^ int(data[b, c])
+            row.append(acc)
+        H.append(row)
+    h = [sum(((H[j][c] >> b) & 1) << c for c in range(cols)) for j in range(m) for b in range(w)]
+    env, y = {}, {}
+
+    def val(tok):
+        tok = tok.strip()
+        if tok.startswith("h["):
+            return h[int(tok[2:-1])]
+        return 0 if tok == "0u" else env[tok]
+
+    for tname, yidx, expr in stmts:
+        v = 0
+        for tok in expr.split("^"):
+            v ^= val(tok)
+        if tname:
+            env[tname] = v
+        else:
+            y[int(yidx)] = v
+    return [[sum(((y[i * w + o] >> c) & 1) << o for o in range(w)) for i in range(m)] for c in range(cols)]
+
+
 def test_generated_networks_match_oracle():
     import gen_networks
     rng = np.random.default_rng(41)
     for (k, m, w, poly, _) in gen_networks.INSTANCES:
+        if w in gen_networks.HORNER_W:
+            data = rng.integers(0, 1 << w, (k, 32))
+            par = horner_parity(k, m, w, poly, data)
+            for c in range(0, 32, 3):
+                assert par[c] == oracle.encode_column([int(v) for v in data[:, c]], m, w, poly), (k, m, w, c)
+            continue
         groups = parse_network(k, m, w, poly)
         cols = 32
         data = rng.integers(0, 1 << w, (k, cols))
