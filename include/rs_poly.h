@@ -130,6 +130,32 @@ rs_status rs_poly_decode_host(const rs_poly_plan *plan, void *host_stripes, size
                               const int32_t *erasures, void *stream, uint64_t *h2d_bytes,
                               uint64_t *d2h_bytes);
 
+/* ---- diff-update ----------------------------------------------------------
+ * The polynomial realization is linear: if data blocks J = data_idx[0..c-1] change
+ * from old to new, then p(new) = p(old) + (x^m * sum_{j in J} (new_j - old_j) x^j mod
+ * g), i.e. p_i ^= sum_{j in J} P[i][j] (old_j ^ new_j) with P the parity map (column
+ * j = x^{m+j} mod g).  The parity blocks are updated IN PLACE; the other data
+ * blocks are not read.  Traffic: (2c + 2m) * block_bytes per stripe.
+ *   data_idx   HOST array of c distinct data indices in [0,k) (any order); c = 0 is a
+ *              no-op; c > k, an index out of range or a duplicate -> RS_ERR_BAD_ERASURE.
+ *   old_data / new_data   HOST arrays of c DEVICE pointers (old_data[i] / new_data[i]
+ *              are the old / new contents of data block data_idx[i]);
+ *   parity     HOST array of m DEVICE pointers, read and overwritten.
+ * Result: bit-identical to rs_poly_encode of the new data (tests pin it to the oracle). */
+rs_status rs_poly_update(const rs_poly_plan *plan, const int *data_idx, int n_changed,
+                         const void *const *old_data, const void *const *new_data,
+                         void *const *parity, size_t block_bytes, void *stream);
+
+/* Batched diff-update: `stripes` ([S][n][B] as in rs_poly_encode_batch) holds the NEW
+ * data (already in place) and the OLD parity, which is updated in place; the old
+ * contents of the changed blocks are in `old_blocks` at old_blocks + s*old_stripe_stride
+ * + i*old_block_stride for block data_idx[i] of stripe s.  The same data_idx for every
+ * stripe. */
+rs_status rs_poly_update_batch(const rs_poly_plan *plan, void *stripes, size_t n_stripes,
+                               size_t stripe_stride, size_t block_stride, size_t block_bytes,
+                               const int *data_idx, int n_changed, const void *old_blocks,
+                               size_t old_stripe_stride, size_t old_block_stride, void *stream);
+
 /* ---- run-time specialised kernels (JIT) ----------------------------------------
  * For every erasure pattern E the decode map survivors -> erased symbols is a fixed
  * GF(2)-linear map (R_E = V_E^{-1} A_E, the paper's Step 1 + Step 2 with Opt1/Opt3
@@ -172,6 +198,10 @@ rs_status rs_poly_plan_stats(const rs_poly_plan *plan, rs_poly_stats *out);
  * bytes (NUL-terminated when cap > 0) into buf and returns the full length, or 0 if
  * the arguments are invalid or the pattern is not JIT-eligible.  Host only. */
 size_t rs_poly_jit_source(const rs_poly_plan *plan, const int *erasures, int n_erasures, char *buf, size_t cap);
+
+/* Same for the diff-update kernel of the changed-block set data_idx[0..c-1] (c >= 1). */
+size_t rs_poly_update_jit_source(const rs_poly_plan *plan, const int *data_idx, int n_changed, char *buf,
+                                 size_t cap);
 
 /* ---- misc ----------------------------------------------------------------- */
 const char *rs_poly_strerror(rs_status status);

@@ -171,6 +171,14 @@ __device__ __forceinline__ void load_unit(const uint8_t *p, uint32_t *x) {
   ldg_v8(p, x);
   if (W == 16) ldg_v8(p + 32, x + 8);
 }
+// y ^= the raw bytes of a unit (an input added unchanged to one output, after transpose back)
+template <int W>
+__device__ __forceinline__ void xor_unit(uint32_t *y, const uint8_t *p) {
+  uint32_t r[W];
+  load_unit<W>(p, r);
+#pragma unroll
+  for (int q = 0; q < W; ++q) y[q] ^= r[q];
+}
 template <int W>
 __device__ __forceinline__ void store_unit(uint8_t *p, const uint32_t *x) {
   stg_v8(p, x);

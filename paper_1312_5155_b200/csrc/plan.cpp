@@ -48,6 +48,17 @@ struct PatternHost {
 
 using MaskKey = std::array<uint64_t, 4>;
 
+// Diff-update of one changed-block set J (sorted): per stripe the kernels see
+// nv = 2c + m virtual blocks, interleaved [new_0, old_0, new_1, old_1, ..., parity_0..m-1],
+// and compute parity_i <- sum_j P[i][j] (new_j + old_j) + parity_i, i.e. M = [P_J P_J | I].
+struct UpdateHost {
+  std::vector<int> idx;     // changed data indices, ascending
+  int nv = 0;
+  std::vector<uint32_t> M;  // m x nv
+  rsb::GenericPat gp{};
+  std::vector<uint8_t> tab;
+};
+
 // A run-time specialised kernel (jit.cpp), compiled once per pattern.
 struct JitEntry {
   std::shared_future<std::shared_ptr<rsb::jit::Kernel>> fut;
@@ -117,6 +128,7 @@ struct rs_poly_plan {
   std::vector<uint8_t> enc_tab;
   mutable std::mutex mu;
   mutable std::map<MaskKey, std::shared_ptr<const PatternHost>> cache;
+  mutable std::map<MaskKey, std::shared_ptr<const UpdateHost>> upd_cache;  // diff-update sets
   // run-time specialised kernels: decode patterns (key = erased mask) and, for codes
   // without a compiled network, the encoder (key = kEncodeKey)
   int jit_mode = RS_JIT_BACKGROUND;
@@ -643,6 +655,109 @@ rs_status collect_patterns(const rs_poly_plan *P, const std::vector<std::vector<
   return RS_OK;
 }
 
+// ---- diff-update ----------------------------------------------------
+MaskKey update_key(const std::vector<int> &idx) {
+  MaskKey key{0, 0, 0, 1ull << 63};  // bit 255 is never an API block (n <= 255): tags the update space
+  for (int j : idx) key[j >> 6] |= 1ull << (j & 63);
+  return key;
+}
+
+std::shared_ptr<const UpdateHost> update_host(const rs_poly_plan &P, const std::vector<int> &idx) {
+  const MaskKey key = update_key(idx);
+  std::lock_guard<std::mutex> lock(P.mu);
+  auto it = P.upd_cache.find(key);
+  if (it != P.upd_cache.end()) return it->second;
+  auto uh = std::make_shared<UpdateHost>();
+  const int c = (int)idx.size(), m = P.m, k = P.k;
+  uh->idx = idx;
+  uh->nv = 2 * c + m;
+  uh->M.assign((size_t)m * uh->nv, 0);
+  for (int i = 0; i < m; ++i) {
+    for (int q = 0; q < c; ++q) {
+      const uint32_t coef = P.pmap[(size_t)i * k + idx[q]];  // x^{m+j} mod g, coefficient of x^i
+      uh->M[(size_t)i * uh->nv + 2 * q] = coef;      // new_j
+      uh->M[(size_t)i * uh->nv + 2 * q + 1] = coef;  // old_j (char 2: + = -)
+    }
+    uh->M[(size_t)i * uh->nv + 2 * c + i] = 1;       // the old parity itself
+  }
+  std::memset(&uh->gp, 0, sizeof(uh->gp));
+  uh->gp.n_in = uh->nv;
+  uh->gp.n_out = m;
+  for (int v = 0; v < uh->nv; ++v) uh->gp.in_blk[v] = (uint8_t)v;
+  for (int i = 0; i < m; ++i) uh->gp.out_blk[i] = (uint8_t)(2 * c + i);
+  pack_generic_tables(P.F, P.w, uh->M, m, uh->nv, uh->tab);
+  P.upd_cache.emplace(key, uh);
+  return uh;
+}
+
+rsb::jit::Spec update_spec(const rs_poly_plan &P, const UpdateHost &uh) {
+  std::vector<int> in(uh.nv), out(P.m);
+  for (int v = 0; v < uh.nv; ++v) in[v] = v;
+  for (int i = 0; i < P.m; ++i) out[i] = 2 * (int)uh.idx.size() + i;
+  rsb::jit::Spec s = jit_spec(P, in, out, uh.M);
+  s.group_blocks = P.w == 8 ? 12 : 4;  // even: each (new_j, old_j) pair shares a CSE group
+  return s;
+}
+
+// ptrs: host [S][nv] virtual block addresses.  Parity is updated in place.
+rs_status update_impl(const rs_poly_plan *P, const UpdateHost &uh, const std::vector<uint64_t> &ptrs,
+                      size_t n_stripes, size_t B, cudaStream_t st) {
+  Geometry G;
+  G.L.base = nullptr;
+  G.L.n = uh.nv;
+  G.n_stripes = n_stripes;
+  G.block_bytes = B;
+  G.aligned32 = G.aligned16 = true;
+  for (uint64_t a : ptrs) {
+    G.aligned32 = G.aligned32 && ptr_aligned(a, 32);
+    G.aligned16 = G.aligned16 && ptr_aligned(a, 16);
+  }
+  uint64_t body = body_units_of(*P, G);
+  const rsb::jit::Kernel *jk = nullptr;
+  if (body && jit_eligible(*P, P->m))
+    jk = jit_get(*P, update_key(uh.idx), [&] { return update_spec(*P, uh); }, false);
+  if (!jk) body = 0;
+  Blob b;
+  const size_t ptrs_off = b.add(ptrs.data(), sizeof(uint64_t) * ptrs.size());
+  rsb::GenericPat gp = uh.gp;
+  gp.table_off = 0;
+  const size_t pats_off = b.add(&gp, sizeof(gp));
+  const size_t tables_off = b.add(uh.tab.data(), uh.tab.size());
+  DevBlob d;
+  cudaError_t e = d.upload(*P, b, st);
+  if (e == cudaSuccess) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
+  if (e == cudaSuccess && body) {
+    e = launch_jit(*jk, G, nullptr, G.n_stripes, body, st);
+    P->jit_launches++;
+  }
+  const uint64_t UB = 32ull * (uint64_t)P->w / 8;
+  if (e == cudaSuccess)
+    e = launch_generic_range(*P, G, body * UB, G.block_bytes, d.p, pats_off, SIZE_MAX, tables_off,
+                             (uint32_t)((P->m + 3) / 4), (uint32_t)(uh.nv * (P->w == 8 ? 128 : 512)), st);
+  cudaError_t ef = d.release();
+  return cuda_status(e != cudaSuccess ? e : ef);
+}
+
+// Validates data_idx; returns the permutation sorting it (order[q] = caller position).
+rs_status parse_update(const rs_poly_plan *P, const int *data_idx, int c, std::vector<int> &sorted,
+                       std::vector<int> &order) {
+  sorted.clear();
+  order.clear();
+  if (c < 0 || (c && !data_idx)) return RS_ERR_INVALID_ARG;
+  if (c > P->k) return RS_ERR_BAD_ERASURE;
+  if (2 * c + P->m > RS_POLY_MAX_N) return RS_ERR_INVALID_ARG;
+  std::vector<char> seen(P->k, 0);
+  for (int q = 0; q < c; ++q) {
+    const int j = data_idx[q];
+    if (j < 0 || j >= P->k || seen[j]) return RS_ERR_BAD_ERASURE;
+    seen[j] = 1;
+    order.push_back(q);
+  }
+  std::sort(order.begin(), order.end(), [&](int a, int b2) { return data_idx[a] < data_idx[b2]; });
+  for (int q : order) sorted.push_back(data_idx[q]);
+  return RS_OK;
+}
+
 const rsb::jit::Kernel *pattern_jit(const rs_poly_plan &P, const PatternHost &ph, const MaskKey &key, bool wait) {
   if (!jit_eligible(P, (int)ph.erased.size())) return nullptr;
   return jit_get(P, key, [&] { return decoder_spec(P, ph); }, wait);
@@ -918,6 +1033,76 @@ size_t rs_poly_jit_source(const rs_poly_plan *P, const int *erasures, int n_eras
     spec = decoder_spec(*P, *ph);
   }
   const std::string s = rsb::jit::source(P->F, spec, nullptr);
+  if (buf && cap) {
+    const size_t nc = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), nc);
+    buf[nc] = 0;
+  }
+  return s.size();
+}
+
+rs_status rs_poly_update(const rs_poly_plan *P, const int *data_idx, int n_changed, const void *const *old_data,
+                         const void *const *new_data, void *const *parity, size_t block_bytes, void *stream) {
+  if (!P) return RS_ERR_INVALID_ARG;
+  std::vector<int> idx, order;
+  rs_status rc = parse_update(P, data_idx, n_changed, idx, order);
+  if (rc) return rc;
+  rc = check_geometry(P, block_bytes);
+  if (rc) return rc;
+  if (n_changed == 0) return RS_OK;
+  if (!old_data || !new_data || !parity) return RS_ERR_INVALID_ARG;
+  const uint64_t a = (uint64_t)(P->w / 8);
+  std::vector<uint64_t> ptrs;
+  for (int q : order) {
+    ptrs.push_back(reinterpret_cast<uint64_t>(new_data[q]));
+    ptrs.push_back(reinterpret_cast<uint64_t>(old_data[q]));
+  }
+  for (int i = 0; i < P->m; ++i) ptrs.push_back(reinterpret_cast<uint64_t>(parity[i]));
+  for (uint64_t v : ptrs)
+    if (!v) return RS_ERR_INVALID_ARG;
+    else if (v % a) return RS_ERR_GEOMETRY;
+  auto uh = update_host(*P, idx);
+  return update_impl(P, *uh, ptrs, 1, block_bytes, static_cast<cudaStream_t>(stream));
+}
+
+rs_status rs_poly_update_batch(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
+                               size_t block_stride, size_t block_bytes, const int *data_idx, int n_changed,
+                               const void *old_blocks, size_t old_stripe_stride, size_t old_block_stride,
+                               void *stream) {
+  if (!P) return RS_ERR_INVALID_ARG;
+  std::vector<int> idx, order;
+  rs_status rc = parse_update(P, data_idx, n_changed, idx, order);
+  if (rc) return rc;
+  rc = check_strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
+  if (rc) return rc;
+  if (n_changed == 0 || n_stripes == 0) return RS_OK;
+  const uint64_t a = (uint64_t)(P->w / 8);
+  if (!old_blocks) return RS_ERR_INVALID_ARG;
+  if (reinterpret_cast<uint64_t>(old_blocks) % a || old_stripe_stride % a || old_block_stride % a)
+    return RS_ERR_GEOMETRY;
+  if (n_changed > 1 && old_block_stride < block_bytes) return RS_ERR_GEOMETRY;
+  if (n_stripes > 1 && old_stripe_stride < (uint64_t)(n_changed - 1) * old_block_stride + block_bytes)
+    return RS_ERR_GEOMETRY;
+  auto uh = update_host(*P, idx);
+  std::vector<uint64_t> ptrs;
+  ptrs.reserve(n_stripes * (size_t)uh->nv);
+  const uint64_t base = reinterpret_cast<uint64_t>(stripes), obase = reinterpret_cast<uint64_t>(old_blocks);
+  for (size_t s = 0; s < n_stripes; ++s) {
+    for (int q : order) {
+      ptrs.push_back(base + s * stripe_stride + (uint64_t)data_idx[q] * block_stride);
+      ptrs.push_back(obase + s * old_stripe_stride + (uint64_t)q * old_block_stride);
+    }
+    for (int i = 0; i < P->m; ++i) ptrs.push_back(base + s * stripe_stride + (uint64_t)(P->k + i) * block_stride);
+  }
+  return update_impl(P, *uh, ptrs, n_stripes, block_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t rs_poly_update_jit_source(const rs_poly_plan *P, const int *data_idx, int n_changed, char *buf,
+                                 size_t cap) {
+  if (!P || n_changed < 1 || !jit_eligible(*P, P->m)) return 0;
+  std::vector<int> idx, order;
+  if (parse_update(P, data_idx, n_changed, idx, order)) return 0;
+  const std::string s = rsb::jit::source(P->F, update_spec(*P, *update_host(*P, idx)), nullptr);
   if (buf && cap) {
     const size_t nc = std::min(cap - 1, s.size());
     std::memcpy(buf, s.data(), nc);

@@ -42,6 +42,10 @@ _lib.rs_poly_prepare.argtypes = [_vp, _vp, _sz]
 _lib.rs_poly_plan_stats.argtypes = [_vp, _vp]
 _lib.rs_poly_jit_source.argtypes = [_vp, _vp, _i32, ctypes.c_char_p, _sz]
 _lib.rs_poly_jit_source.restype = _sz
+_lib.rs_poly_update.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]
+_lib.rs_poly_update_batch.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _i32, _vp, _sz, _sz, _vp]
+_lib.rs_poly_update_jit_source.argtypes = [_vp, _vp, _i32, ctypes.c_char_p, _sz]
+_lib.rs_poly_update_jit_source.restype = _sz
 
 
 class Stats(ctypes.Structure):
@@ -211,6 +215,40 @@ class Plan:
         er = _erasure_table(erasures, S, self.m)
         _check(_lib.rs_poly_decode_batch(self._h, ptr, S, ss, bs, B, er.ctypes.data, _stream(stream)),
                "rs_poly_decode_batch")
+
+    # ---- diff-update ----------------------------------------------------
+    def update(self, data_idx, old_data, new_data, parity, block_bytes: int, stream=None) -> None:
+        """parity ^= P[:, data_idx] (old ^ new), in place (rs_poly_update)."""
+        idx = list(data_idx)
+        c = len(idx)
+        ix = (ctypes.c_int * max(1, c))(*idx)
+        o = (ctypes.c_void_p * max(1, c))(*[_ptr(x) for x in old_data])
+        nw = (ctypes.c_void_p * max(1, c))(*[_ptr(x) for x in new_data])
+        p = (ctypes.c_void_p * self.m)(*[_ptr(x) for x in parity])
+        _check(_lib.rs_poly_update(self._h, ix, c, o, nw, p, block_bytes, _stream(stream)), "rs_poly_update")
+
+    def update_batch(self, stripes, data_idx, old_blocks, stream=None) -> None:
+        """stripes [S][n][B]: new data + old parity (updated in place); old_blocks [S][c][B]."""
+        ptr, S, ss, bs, B = _geometry(stripes, self.n)
+        idx = list(data_idx)
+        c = len(idx)
+        ix = (ctypes.c_int * max(1, c))(*idx)
+        shape = tuple(old_blocks.shape)
+        if c and (len(shape) != 3 or shape[0] != S or shape[1] != c or shape[2] != B):
+            raise ValueError(f"old_blocks must be [{S}][{c}][{B}]")
+        ost = old_blocks.stride() if hasattr(old_blocks, "stride") else old_blocks.strides
+        _check(_lib.rs_poly_update_batch(self._h, ptr, S, ss, bs, B, ix, c, _ptr(old_blocks), ost[0], ost[1],
+                                         _stream(stream)), "rs_poly_update_batch")
+
+    def update_jit_source(self, data_idx) -> str:
+        idx = list(data_idx)
+        ix = (ctypes.c_int * max(1, len(idx)))(*idx)
+        n = _lib.rs_poly_update_jit_source(self._h, ix, len(idx), None, 0)
+        if n == 0:
+            return ""
+        buf = ctypes.create_string_buffer(n + 1)
+        _lib.rs_poly_update_jit_source(self._h, ix, len(idx), buf, n + 1)
+        return buf.value.decode()
 
     # ---- end to end from host memory --------------------------------------------
     def encode_host(self, host_stripes, stream=None):

@@ -35,7 +35,10 @@ def parse(src):
         stmts = re.findall(r"^\s+(const uint32_t (t\d+)|y\[(\d+)\]) (\^?=) (.*);$", body, re.M)
         groups.append((loads, stmts))
     stores = [(int(i), int(base)) for i, base in re.findall(r"store_unit<\d+>\(bo(\d+) \+ off, &y\[(\d+)\]\);", src)]
-    return w, ins, outs, groups, stores
+    # pass-through inputs: bytes XORed into an output after its transpose back
+    pins = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bp(\d+) = blkp\(a, s, (\d+)\);", src)}
+    passes = [(int(base), pins[int(i)]) for base, i in re.findall(r"xor_unit<\d+>\(&y\[(\d+)\], bp(\d+) \+ off\);", src)]
+    return w, ins, outs, groups, stores, passes
 
 
 def evaluate_horner(src, cw_cols):
@@ -138,7 +141,7 @@ def evaluate(src, cw_cols):
     """cw_cols: [n][C] symbols (API order).  Returns {out_block: [C] symbols}."""
     if "horner_step<" in src:
         return evaluate_horner(src, cw_cols)
-    w, ins, outs, groups, stores = parse(src)
+    w, ins, outs, groups, stores, passes = parse(src)
     C = cw_cols.shape[1]
     nout = len(outs)
     y = [0] * (nout * w)
@@ -171,6 +174,9 @@ def evaluate(src, cw_cols):
     res = {}
     for i, base in stores:
         res[outs[i]] = [sum(((y[base + o] >> c) & 1) << o for o in range(w)) for c in range(C)]
+        for pbase, blk in passes:
+            if pbase == base:
+                res[outs[i]] = [v ^ int(cw_cols[blk][c]) for c, v in enumerate(res[outs[i]])]
     return res
 
 
@@ -234,3 +240,29 @@ def test_jit_source_compiles_for_sm100a(rs, k, m, w, poly, er):
                              capture_output=True, text=True, timeout=600)
         assert out.returncode == 0, out.stderr[-3000:]
         assert "spill stores" in out.stderr
+
+
+@pytest.mark.parametrize("k,m,w,poly,idx", [(10, 4, 8, P8, [3]), (10, 4, 8, P8, [7, 0, 9]), (6, 3, 8, P8, [5, 1]),
+                                            (12, 4, 16, P16, [11, 2]), (5, 2, 8, P8, list(range(5)))])
+def test_jit_update_network_matches_oracle(rs, k, m, w, poly, idx):
+    """Diff-update: the generated network applied to (new, old, old parity) gives
+    the oracle's encoding of the new data."""
+    plan = rs.Plan(k, m, w, poly)
+    src = plan.update_jit_source(idx)
+    assert src
+    C = 32
+    rng = np.random.default_rng(len(idx) + k)
+    old = rng.integers(0, 1 << w, (k, C))
+    new = old.copy()
+    for j in idx:
+        new[j] = rng.integers(0, 1 << w, C)
+    old_par = np.array([oracle.encode_column([int(v) for v in old[:, c]], m, w, poly) for c in range(C)]).T
+    new_par = np.array([oracle.encode_column([int(v) for v in new[:, c]], m, w, poly) for c in range(C)]).T
+    order = sorted(idx)
+    virt = []                      # [new_0, old_0, new_1, old_1, ..., parity]
+    for j in order:
+        virt += [new[j], old[j]]
+    virt += list(old_par)
+    got = evaluate(src, np.array(virt, dtype=np.int64))
+    for i in range(m):
+        assert got[2 * len(order) + i] == [int(v) for v in new_par[i]]

@@ -1,0 +1,135 @@
+#!/usr/bin/env python3
+"""Measurements for SURVEY §8(f)'s next rows (not the driver's headline line; that is bench.py).
+
+  python tools/bench_next.py update  [--config C5] [--changed 1] [--steps 20] [--warmup 3]
+  python tools/bench_next.py sweep   [--steps 10]          # erasure-count / (k, m) sweeps (NEXT-2)
+
+Each prints one JSON line per measured case: device time with CUDA events on the launching
+stream (inputs resident in HBM, >> L2), algorithmic bytes, fraction of the measured HBM copy
+peak, and the correctness check that preceded the number (oracle on sampled columns).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402  (hbm_peak, ClockSampler)
+import synth  # noqa: E402
+
+SPAN = 64 << 10
+
+
+def sampled_encode_ok(dev_stripes, host_data_fn, c, picks):
+    """Parity of stripes `picks` on the device equals the oracle's encoding of the data
+    host_data_fn(s) (first/last 64 KiB columns)."""
+    import oracle
+    k, m, w, B = c["k"], c["m"], c["w"], c["block_bytes"]
+    span = min(B // 2, SPAN) // (w // 8) * (w // 8)
+    bad = 0
+    for s in picks:
+        host = host_data_fn(s)
+        cols = np.concatenate([host[:, :, :span], host[:, :, B - span:]], axis=2).copy()
+        oracle.encode_bulk(cols, k, m, w, c["poly"], threads=4)
+        got = dev_stripes[s].cpu().numpy()
+        got = np.concatenate([got[None, :, :span], got[None, :, B - span:]], axis=2)
+        bad += int(not np.array_equal(got[:, k:], cols[:, k:]))
+    return bad
+
+
+def timed(fn, steps, warmup, stream):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(stream)
+    for i in range(steps):
+        fn()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    return [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-1: diff-update
+# ---------------------------------------------------------------------------------------
+def run_update(a):
+    import torch
+    import paper_1312_5155_b200 as rsp
+    c = dict(synth.CONFIGS[a.config])
+    c["seed"] = c["seed"] or 0
+    k, m, w, B, S = c["k"], c["m"], c["w"], c["block_bytes"], c["stripes"]
+    n = k + m
+    idx = list(range(k // 2, k // 2 + a.changed)) if a.changed <= k - k // 2 else list(range(a.changed))
+    plan = rsp.Plan(k, m, w, c["poly"])
+    st = torch.empty((S, n, B), dtype=torch.uint8, device="cuda")
+    rsp.synth_fill(st, k, seed=c["seed"])
+    plan.encode_batch(st)                                   # old parity of the old data
+    old = st[:, idx].clone()                                # old contents of the changed blocks
+    newseed = c["seed"] + 1000
+    tmp = torch.empty((S, n, B), dtype=torch.uint8, device="cuda")
+    rsp.synth_fill(tmp, k, seed=newseed)
+    st[:, idx] = tmp[:, idx]                                # new data in place
+    del tmp
+    plan.set_jit(rsp.RS_JIT_SYNC)                           # compile the set's kernel in the first call
+    stream = torch.cuda.current_stream()
+    plan.update_batch(st, idx, old)                         # first call: verified below
+    torch.cuda.synchronize()
+    picks = sorted({0, S // 2, S - 1})
+
+    def new_data(s):
+        h = synth.stripes_array(c["seed"], [s], k, m, B)
+        h2 = synth.stripes_array(newseed, [s], k, m, B)
+        h[:, idx] = h2[:, idx]
+        return h
+
+    def old_data(s):
+        return synth.stripes_array(c["seed"], [s], k, m, B)
+
+    bad = sampled_encode_ok(st, new_data, c, picks)
+    clk = bench.ClockSampler(torch.cuda.current_device()).start()
+    ms = timed(lambda: plan.update_batch(st, idx, old), a.steps, a.warmup, stream)
+    clocks = clk.stop()
+    total = 1 + a.warmup + a.steps                         # each call toggles old <-> new parity
+    bad += sampled_encode_ok(st, new_data if total % 2 else old_data, c, picks)
+    moved = S * (2 * len(idx) + 2 * m) * B
+    avg = statistics.mean(ms)
+    peak, src = bench.hbm_peak()
+    line = {"row": "NEXT-1 diff-update (P:210)", "metric": "changed user data GB/s", "config": a.config,
+            "k": k, "m": m, "w": w, "stripes": S, "block_bytes": B, "changed_blocks": idx,
+            "value": round(S * len(idx) * B / (avg / 1e3) / 1e9, 2), "unit": "GB/s", "ms": round(avg, 4),
+            "roofline": {"bound": "hbm", "achieved": round(moved / (avg / 1e3) / 1e9, 1), "peak": peak,
+                         "frac": round(moved / (avg / 1e3) / 1e9 / peak, 4), "unit": "GB/s",
+                         "traffic_model": "S*(2c+2m)*B: read old+new of c blocks, read+write m parity",
+                         "peak_source": src},
+            "vs_reencode": "re-encoding would move S*(k+m)*B = "
+                           f"{S * (k + m) * B / 1e9:.2f} GB vs {moved / 1e9:.2f} GB",
+            "verified": {"mismatches": bad, "how": "parity vs oracle re-encode of the new data on sampled "
+                                                    "columns of 3 stripes, before and after timing"},
+            "steps": a.steps, "warmup": a.warmup, "clocks": clocks, "jit": plan.stats()["jit_launches"] > 0}
+    print(json.dumps(line), flush=True)
+    return 0 if bad == 0 else 1
+
+
+# ---------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", choices=["update"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--changed", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    a = ap.parse_args()
+    if a.what == "update":
+        return run_update(a)
+    return 2
+
+
+if __name__ == "__main__":
+    sys.exit(main())
