@@ -173,6 +173,19 @@ rs_status rs_poly_update_batch(const rs_poly_plan *plan, void *stripes, size_t n
 #define RS_JIT_SYNC 2
 rs_status rs_poly_plan_set_jit(rs_poly_plan *plan, int mode);
 
+/* Decode read policy.  RS_READ_ALL_SURVIVORS (default, the paper's
+ * method: Step 1 sums over every non-erased position, Opt2 of P:321) reads the n-t
+ * survivors.  RS_READ_K_SURVIVORS reads only k of them (data first) when t < m and
+ * solves the m x m system of the t erased plus m-t unread blocks from all m syndromes:
+ * identical output (the code is MDS), traffic (k+t)*B instead of (k+m)*B per
+ * stripe; the unread survivors may hold anything.  (Under this policy the fallback
+ * for a pattern whose JIT kernel is not ready is the generic kernel, not the
+ * bit-sliced table kernel, which reads every survivor.)  A configuration call: it drops the plan's
+ * decode-pattern cache; make it before sharing the plan. */
+#define RS_READ_ALL_SURVIVORS 0
+#define RS_READ_K_SURVIVORS 1
+rs_status rs_poly_plan_set_read_policy(rs_poly_plan *plan, int policy);
+
 /* Precompute (Opt1/Opt3) the decode constants of every pattern listed in
  * `erasures` (HOST int32 [n_rows][m], -1 padded, as in rs_poly_decode_batch) and,
  * unless JIT is off, compile their kernels, blocking until they are ready.  Also

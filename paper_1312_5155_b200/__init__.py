@@ -8,6 +8,6 @@
 from .rs_poly import (DEFAULT_POLY, LIB_PATH, SYNTH_PATH, Plan, RSError, abi_version, launch_count,  # noqa: F401
                       RS_OK, RS_ERR_INVALID_ARG, RS_ERR_NOT_PRIMITIVE, RS_ERR_GEOMETRY, RS_ERR_TOO_MANY_ERASURES,
                       RS_ERR_BAD_ERASURE, RS_ERR_CUDA, RS_ERR_NOMEM, RS_JIT_OFF, RS_JIT_BACKGROUND, RS_JIT_SYNC,
-                      strerror, synth_fill)
+                      RS_READ_ALL_SURVIVORS, RS_READ_K_SURVIVORS, strerror, synth_fill)
 
 __all__ = ["Plan", "RSError", "synth_fill", "launch_count", "abi_version", "strerror", "DEFAULT_POLY"]

@@ -40,6 +40,10 @@ struct PatternHost {
   std::vector<int> surv;    // survivors, ascending API index (columns of R)
   std::vector<uint32_t> R;  // t x (n-t) decode matrix V_E^{-1} A_E
   std::vector<uint32_t> Vinv;  // t x t, V_E^{-1} (Step 2)
+  // Syndrome-form (w16 JIT) solve: unknowns U (= E, or E + the survivors not read under
+  // RS_READ_K_SURVIVORS), Hm = rows E of V_U^{-1} (t x |U|), |U| syndromes used.
+  std::vector<int> unknown;
+  std::vector<uint32_t> Hm;
   rsb::SlicedPat sp{};
   std::vector<uint8_t> wtab;  // sliced W tables
   rsb::GenericPat gp{};
@@ -132,7 +136,9 @@ struct rs_poly_plan {
   // run-time specialised kernels: decode patterns (key = erased mask) and, for codes
   // without a compiled network, the encoder (key = kEncodeKey)
   int jit_mode = RS_JIT_BACKGROUND;
+  int read_policy = RS_READ_ALL_SURVIVORS;
   mutable std::map<MaskKey, std::shared_ptr<JitEntry>> jit;
+  std::vector<std::shared_ptr<JitEntry>> retired;  // dropped by a policy change, released at destroy
   mutable std::map<int, std::vector<cudaStream_t>> pool;  // device -> side streams for concurrent launches
   mutable std::atomic<uint64_t> jit_launches{0}, table_launches{0};
   // pinned host slots for the per-call constant blob: a pageable cudaMemcpyAsync may
@@ -171,9 +177,10 @@ struct rs_poly_plan {
       }
       if (sl.p) cudaFreeHost(sl.p);
     }
-    for (auto &kv : jit) {
-      if (kv.second->fut.valid()) {
-        auto k = kv.second->fut.get();
+    for (auto &kv : jit) retired.push_back(kv.second);
+    for (auto &e : retired) {
+      if (e->fut.valid()) {
+        auto k = e->fut.get();
         if (k) rsb::jit::release(*k);
       }
     }
@@ -247,6 +254,42 @@ std::shared_ptr<const PatternHost> build_pattern(const rs_poly_plan &P, const st
     }
   ph->surv = surv;
   ph->R = R;
+  ph->unknown = er;
+  ph->Hm = ph->Vinv;
+  if (P.read_policy == RS_READ_K_SURVIVORS && t < m) {
+    // Read only k survivors K (data first, then parity, ascending): the m - t unread ones
+    // join the unknowns U (|U| = m), solved from all m syndrome equations (j < m):
+    // c_U = V_U^{-1} A_K c_K; only the E rows are produced.  Unique (MDS), so the
+    // output is identical; the traffic is (k + t) B instead of (n - t) B + t B.
+    std::vector<int> K, U = er;
+    for (int b = 0; b < n && (int)K.size() < k; ++b)
+      if (!is_er[b]) K.push_back(b);
+    for (int b = 0; b < n; ++b)
+      if (!is_er[b] && std::find(K.begin(), K.end(), b) == K.end()) U.push_back(b);
+    std::sort(U.begin(), U.end());
+    std::vector<uint32_t> VU((size_t)m * m);
+    for (int j = 0; j < m; ++j)
+      for (int u = 0; u < m; ++u)
+        VU[(size_t)j * m + u] =
+            F.alpha_pow((uint64_t)rsb::position(U[u], k, m) * (uint64_t)j);
+    if (!rsb::invert(F, VU, m)) return nullptr;
+    std::vector<int> rowE;  // row of V_U^{-1} for each erased block, in er order
+    for (int b : er) rowE.push_back((int)(std::find(U.begin(), U.end(), b) - U.begin()));
+    std::vector<uint32_t> RK((size_t)t * k, 0), Hm((size_t)t * m, 0);
+    for (int e = 0; e < t; ++e) {
+      for (int u = 0; u < m; ++u) Hm[(size_t)e * m + u] = VU[(size_t)rowE[e] * m + u];
+      for (int q = 0; q < k; ++q) {
+        uint32_t acc = 0;
+        const uint64_t p = (uint64_t)rsb::position(K[q], k, m);
+        for (int j = 0; j < m; ++j) acc ^= F.mul(Hm[(size_t)e * m + j], F.alpha_pow((uint64_t)j * p));
+        RK[(size_t)e * k + q] = acc;
+      }
+    }
+    ph->surv = K;
+    ph->R = RK;
+    ph->unknown = U;
+    ph->Hm = Hm;
+  }
   // sliced record
   if (P.sliced) {
     std::memset(&ph->sp, 0, sizeof(ph->sp));
@@ -257,11 +300,12 @@ std::shared_ptr<const PatternHost> build_pattern(const rs_poly_plan &P, const st
   }
   // generic record
   std::memset(&ph->gp, 0, sizeof(ph->gp));
-  ph->gp.n_in = ns;
+  const int nin = (int)ph->surv.size();
+  ph->gp.n_in = nin;
   ph->gp.n_out = t;
-  for (int si = 0; si < ns; ++si) ph->gp.in_blk[si] = (uint8_t)surv[si];
+  for (int si = 0; si < nin; ++si) ph->gp.in_blk[si] = (uint8_t)ph->surv[si];
   for (int e = 0; e < t; ++e) ph->gp.out_blk[e] = (uint8_t)er[e];
-  pack_generic_tables(F, P.w, R, t, ns, ph->rtab);
+  pack_generic_tables(F, P.w, ph->R, t, nin, ph->rtab);
   return ph;
 }
 
@@ -343,10 +387,10 @@ rsb::jit::Spec decoder_spec(const rs_poly_plan &P, const PatternHost &ph) {
   if (P.w == 16) {
     s.horner = true;
     s.poly = P.poly;
-    s.T = (int)ph.erased.size();
-    s.M = ph.Vinv;
+    s.T = (int)ph.unknown.size();
+    s.M = ph.Hm;
     std::vector<char> er(P.n, 0);
-    for (int b : ph.erased) er[b] = 1;
+    for (int b : ph.unknown) er[b] = 1;
     for (int pos = P.n - 1; pos >= 0; --pos) {
       const int b = pos >= P.m ? pos - P.m : P.k + pos;  // inverse of rsb::position
       s.seq.push_back(er[b] ? -1 : b);
@@ -782,7 +826,9 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
       jk[i] = pattern_jit(*P, *pats[i], keys[i], false);
       any_jit = any_jit || jk[i];
     }
-  if (!P->sliced && !any_jit) body = 0;
+  // the table-driven bit-sliced decode reads every survivor: not under RS_READ_K_SURVIVORS
+  const bool sliced_rt = P->sliced && P->read_policy == RS_READ_ALL_SURVIVORS;
+  if (!sliced_rt && !any_jit) body = 0;
   std::vector<int32_t> idx_rt(idx);
   std::vector<std::vector<int32_t>> groups(pats.size());
   bool any_rt = false;
@@ -829,7 +875,7 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   if (e == cudaSuccess && ptrs) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
   // table-driven body for stripes without a ready JIT kernel
   if (e == cudaSuccess && body && any_rt) {
-    if (P->sliced) e = launch_sliced_body(*P, true, G, body, d.p, sliced_pats_off, idx_rt_off, tables_off, st);
+    if (sliced_rt) e = launch_sliced_body(*P, true, G, body, d.p, sliced_pats_off, idx_rt_off, tables_off, st);
     else e = launch_generic_range(*P, G, 0, body * UB, d.p, generic_pats_off, idx_rt_off, tables_off, max_groups,
                                   smem, st);
     P->table_launches++;
@@ -982,6 +1028,23 @@ void rs_poly_plan_destroy(rs_poly_plan *plan) { delete plan; }
 rs_status rs_poly_plan_set_jit(rs_poly_plan *P, int mode) {
   if (!P || mode < RS_JIT_OFF || mode > RS_JIT_SYNC) return RS_ERR_INVALID_ARG;
   P->jit_mode = mode;
+  return RS_OK;
+}
+
+rs_status rs_poly_plan_set_read_policy(rs_poly_plan *P, int policy) {
+  if (!P || (policy != RS_READ_ALL_SURVIVORS && policy != RS_READ_K_SURVIVORS)) return RS_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> lock(P->mu);
+  if (P->read_policy == policy) return RS_OK;
+  P->read_policy = policy;
+  P->cache.clear();
+  for (auto it = P->jit.begin(); it != P->jit.end();) {
+    if ((it->first[3] >> 63) == 0) {  // erasure-pattern kernels (encode/update keys carry bit 255)
+      P->retired.push_back(it->second);
+      it = P->jit.erase(it);
+    } else {
+      ++it;
+    }
+  }
   return RS_OK;
 }
 

@@ -38,6 +38,7 @@ _lib.rs_poly_strerror.argtypes = [_i32]
 _lib.rs_poly_strerror.restype = ctypes.c_char_p
 _lib.rs_poly_abi_version.restype = _i32
 _lib.rs_poly_plan_set_jit.argtypes = [_vp, _i32]
+_lib.rs_poly_plan_set_read_policy.argtypes = [_vp, _i32]
 _lib.rs_poly_prepare.argtypes = [_vp, _vp, _sz]
 _lib.rs_poly_plan_stats.argtypes = [_vp, _vp]
 _lib.rs_poly_jit_source.argtypes = [_vp, _vp, _i32, ctypes.c_char_p, _sz]
@@ -58,6 +59,7 @@ class Stats(ctypes.Structure):
 
 
 RS_JIT_OFF, RS_JIT_BACKGROUND, RS_JIT_SYNC = 0, 1, 2
+RS_READ_ALL_SURVIVORS, RS_READ_K_SURVIVORS = 0, 1
 _lib.rs_poly_launch_count.restype = _u64
 
 RS_OK, RS_ERR_INVALID_ARG, RS_ERR_NOT_PRIMITIVE, RS_ERR_GEOMETRY = 0, 1, 2, 3
@@ -160,6 +162,10 @@ class Plan:
     def set_jit(self, mode: int) -> None:
         """RS_JIT_OFF / RS_JIT_BACKGROUND (default) / RS_JIT_SYNC."""
         _check(_lib.rs_poly_plan_set_jit(self._h, mode), "rs_poly_plan_set_jit")
+
+    def set_read_policy(self, policy: int) -> None:
+        """RS_READ_ALL_SURVIVORS (default, the paper's Step 1) / RS_READ_K_SURVIVORS."""
+        _check(_lib.rs_poly_plan_set_read_policy(self._h, policy), "rs_poly_plan_set_read_policy")
 
     def prepare(self, erasures) -> None:
         """Precompute decode constants and compile JIT kernels for these patterns ([rows][m], -1 padded)."""

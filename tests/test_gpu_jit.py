@@ -108,3 +108,39 @@ def test_jit_encoder_for_codes_without_compiled_network(k, m, w, poly):
     torch.cuda.synchronize()
     assert np.array_equal(d.cpu().numpy(), ref)
     assert plan.stats()["jit_launches"] == 1
+
+
+@pytest.mark.parametrize("jit", [True, False])
+@pytest.mark.parametrize("k,m,w,poly,B", [(10, 4, 8, P8, 64 * 1024 + 40), (12, 4, 16, P16, 32 * 1024 + 6),
+                                          (6, 3, 8, P8, 8192), (10, 6, 8, P8, 4096)])
+def test_k_survivor_read_policy(k, m, w, poly, B, jit):
+    """RS_READ_K_SURVIVORS (NEXT-2): only k survivors are read when t < m; the unread
+    survivors are overwritten with garbage first to prove they are not used."""
+    S, n = 10, k + m
+    ref = encoded(k, m, w, poly, B, S, seed=25)
+    rng = np.random.default_rng(k * 7 + m)
+    er = np.full((S, m), -1, dtype=np.int32)
+    for s in range(S):
+        t = 1 + (s % m)
+        er[s, :t] = rng.choice(n, t, replace=False)
+    m_ = rs()
+    plan = m_.Plan(k, m, w, poly)
+    plan.set_read_policy(m_.RS_READ_K_SURVIVORS)
+    plan.set_jit(m_.RS_JIT_SYNC if jit else m_.RS_JIT_OFF)
+    bad = ref.copy()
+    for s in range(S):
+        e = [b for b in er[s] if b >= 0]
+        for b in e:
+            bad[s, b] = 0x3C
+        # the k survivors read are the first k non-erased blocks (data first); scribble the rest
+        surv = [b for b in range(n) if b not in e]
+        for b in surv[k:]:
+            bad[s, b] = 0x77
+    d = torch.from_numpy(bad).cuda()
+    plan.decode_batch(d, er)
+    torch.cuda.synchronize()
+    got = d.cpu().numpy()
+    for s in range(S):
+        for b in er[s]:
+            if b >= 0:
+                assert np.array_equal(got[s, b], ref[s, b]), (s, b)

@@ -189,10 +189,13 @@ def codewords(k, m, w, poly, C, seed):
     return cols
 
 
+@pytest.mark.parametrize("policy", [0, 1])
 @pytest.mark.parametrize("k,m,w,poly", [(10, 4, 8, P8), (6, 3, 8, P8), (12, 4, 16, P16), (5, 2, 8, P8),
                                         (10, 6, 8, P8), (20, 8, 8, P8)])
-def test_jit_decode_networks_match_oracle(rs, k, m, w, poly):
+def test_jit_decode_networks_match_oracle(rs, k, m, w, poly, policy):
+    """policy 0: every survivor read (the paper's Step 1); 1: only k survivors read (NEXT-2)."""
     plan = rs.Plan(k, m, w, poly)
+    plan.set_read_policy(policy)
     n = k + m
     rng = np.random.default_rng(k * 31 + m)
     cols = codewords(k, m, w, poly, 32, seed=k + m)
@@ -210,6 +213,8 @@ def test_jit_decode_networks_match_oracle(rs, k, m, w, poly):
         assert sorted(got) == sorted(er)
         for b in er:
             assert got[b] == [int(v) for v in cols[b]], (er, b)
+        reads = set(re.findall(r"blkp\(a, s, (\d+)\)", src)) - {str(b) for b in er}
+        assert len(reads) == (k if policy == 1 else k + m - len(er)), (er, sorted(reads))
 
 
 @pytest.mark.parametrize("k,m,w,poly", [(5, 2, 8, P8), (10, 6, 8, P8), (10, 4, 16, P16), (3, 1, 8, P8)])

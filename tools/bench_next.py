@@ -118,9 +118,83 @@ def run_update(a):
 
 
 # ---------------------------------------------------------------------------------------
+# NEXT-2: erasure-count, k, m and block-size sweeps (the paper's Figs 1-4) and
+# the k-survivor read policy
+# ---------------------------------------------------------------------------------------
+def sweep_point(k, m, B, S, t, policy, steps, warmup, fig, w=8, poly=0x11D, seed=0):
+    import torch
+    import paper_1312_5155_b200 as rsp
+    n = k + m
+    plan = rsp.Plan(k, m, w, poly)
+    plan.set_read_policy(policy)
+    st = torch.empty((S, n, B), dtype=torch.uint8, device="cuda")
+    rsp.synth_fill(st, k, seed=seed)
+    er = np.full((S, m), -1, dtype=np.int32)
+    for s in range(S):
+        er[s, :t] = synth.erasure_draw(seed, s, range(n), t)
+    plan.prepare(er)
+    stream = torch.cuda.current_stream()
+    plan.encode_batch(st)
+    torch.cuda.synchronize()
+    c = {"k": k, "m": m, "w": w, "block_bytes": B, "poly": poly}
+    picks = sorted({0, S - 1})
+    bad = sampled_encode_ok(st, lambda s_: synth.stripes_array(seed, [s_], k, m, B), c, picks)
+    golden = st.clone()
+    for s in range(S):
+        st[s, torch.from_numpy(er[s, :t].astype(np.int64)).cuda()] = 0xEE
+    plan.decode_batch(st, er)
+    torch.cuda.synchronize()
+    bad += 0 if torch.equal(st, golden) else 1
+    del golden
+    torch.cuda.empty_cache()
+    enc = statistics.mean(timed(lambda: plan.encode_batch(st), steps, warmup, stream))
+    dec = statistics.mean(timed(lambda: plan.decode_batch(st, er), steps, warmup, stream))
+    peak, _ = bench.hbm_peak()
+    user = S * k * B
+    moved_enc = S * n * B
+    moved_dec = S * ((k + t) if (policy == 1 and t < m) else n) * B
+    return {"row": "NEXT-2 sweep", "figure": fig, "k": k, "m": m, "w": w, "block_bytes": B, "stripes": S,
+            "erasures": t, "read_policy": ["all_survivors", "k_survivors"][policy],
+            "encode": {"gbs_user": round(user / enc / 1e6, 1), "ms": round(enc, 4),
+                       "hbm_frac": round(moved_enc / enc / 1e6 / peak, 4)},
+            "decode": {"gbs_user": round(user / dec / 1e6, 1), "ms": round(dec, 4),
+                       "hbm_frac": round(moved_dec / dec / 1e6 / peak, 4), "bytes_moved": moved_dec},
+            "verified": {"mismatches": bad, "how": "encode vs oracle on sampled columns of 2 stripes; decode "
+                                                    "restores every erased byte (device compare)"},
+            "jit": plan.stats()["jit_launches"] > 0}
+
+
+def run_sweep(a):
+    MiB = 1 << 20
+    data_target = a.data_gib << 30
+    pts = []
+    # Fig. 2: RS(10,4), 4 MB blocks, 1..4 erasures -- both read policies
+    for t in (1, 2, 3, 4):
+        for pol in (0, 1):
+            pts.append(dict(k=10, m=4, B=4 * MiB, t=t, policy=pol, fig="Fig2 erasures"))
+    # Fig. 1: block size 1..4 MB, RS(10,4), 4 erasures
+    for mb in (1, 2, 3):
+        pts.append(dict(k=10, m=4, B=mb * MiB, t=4, policy=0, fig="Fig1 block size"))
+    # Fig. 3: k sweep at m = 4
+    for k in (6, 8, 12):
+        pts.append(dict(k=k, m=4, B=4 * MiB, t=4, policy=0, fig="Fig3 k"))
+    # Fig. 4: m sweep at k = 10 (m = 5, 6 use the JIT encoder)
+    for m in (2, 3, 5, 6):
+        pts.append(dict(k=10, m=m, B=4 * MiB, t=m, policy=0, fig="Fig4 m"))
+    bad = 0
+    for p in pts:
+        S = max(1, data_target // (p["k"] * p["B"]))
+        r = sweep_point(p["k"], p["m"], p["B"], S, p["t"], p["policy"], a.steps, a.warmup, p["fig"])
+        bad += r["verified"]["mismatches"]
+        print(json.dumps(r), flush=True)
+    return 0 if bad == 0 else 1
+
+
+# ---------------------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["update"])
+    ap.add_argument("what", choices=["update", "sweep"])
+    ap.add_argument("--data-gib", type=int, default=20, help="sweep: user data per point")
     ap.add_argument("--config", default="C5")
     ap.add_argument("--changed", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -128,6 +202,8 @@ def main():
     a = ap.parse_args()
     if a.what == "update":
         return run_update(a)
+    if a.what == "sweep":
+        return run_sweep(a)
     return 2
 
 
