@@ -144,7 +144,9 @@ def evaluate(src, cw_cols):
     w, ins, outs, groups, stores, passes = parse(src)
     C = cw_cols.shape[1]
     nout = len(outs)
-    y = [0] * (nout * w)
+    # y starts undefined unless the source zeroes it: a read of an unset plane fails
+    zero = re.search(r"for \(int q = 0; q < \d+; \+\+q\) y\[q\] = 0u;", src) is not None
+    y = [0 if zero else None] * (nout * w)
     for loads, stmts in groups:
         x = {}
         for i, base in loads:
@@ -170,9 +172,11 @@ def evaluate(src, cw_cols):
             elif op == "=":
                 y[int(yidx)] = v
             else:
+                assert y[int(yidx)] is not None, "accumulating into an unset output plane"
                 y[int(yidx)] ^= v
     res = {}
     for i, base in stores:
+        assert all(y[base + o] is not None for o in range(w)), "storing an unset output plane"
         res[outs[i]] = [sum(((y[base + o] >> c) & 1) << o for o in range(w)) for c in range(C)]
         for pbase, blk in passes:
             if pbase == base:
