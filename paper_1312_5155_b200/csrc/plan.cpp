@@ -149,7 +149,9 @@ struct rs_poly_plan {
     int dev = 0;
     cudaEvent_t ev = nullptr;
     bool busy = false;
+    uint64_t seq = 0;  // order of last use
   };
+  mutable uint64_t stage_seq = 0;
   mutable std::mutex stage_mu;
   mutable std::vector<PinnedSlot> stage;
   // device staging of the host entry points (rs_poly_*_host), one per device, reused
@@ -570,7 +572,10 @@ cudaError_t launch_generic_range(const rs_poly_plan &P, const Geometry &G, uint6
 // Copy `bytes` at `src` to device `dst` on stream `s` through one of the plan's pinned
 // slots (reused once its previous copy has completed); pageable only if no slot can be had.
 cudaError_t upload_pinned(const rs_poly_plan &P, void *dst, const void *src, size_t bytes, cudaStream_t s) {
-  constexpr size_t kMaxSlots = 64;
+  // At most kMaxSlots pinned slots.  When all are in flight the host is at least that
+  // many calls ahead of the GPU, so it waits for the oldest copy instead of allocating:
+  // a cudaHostAlloc inside a stream of back-to-back calls can starve the GPU.
+  constexpr size_t kMaxSlots = 16;
   int dev = 0;
   cudaGetDevice(&dev);
   rs_poly_plan::PinnedSlot *slot = nullptr;
@@ -581,6 +586,12 @@ cudaError_t upload_pinned(const rs_poly_plan &P, void *dst, const void *src, siz
         slot = &sl;
         break;
       }
+    if (!slot && P.stage.size() >= kMaxSlots) {
+      rs_poly_plan::PinnedSlot *oldest = nullptr;
+      for (auto &sl : P.stage)
+        if (!sl.busy && sl.dev == dev && sl.cap >= bytes && (!oldest || sl.seq < oldest->seq)) oldest = &sl;
+      if (oldest && cudaEventSynchronize(oldest->ev) == cudaSuccess) slot = oldest;
+    }
     if (!slot && P.stage.size() < kMaxSlots) {
       rs_poly_plan::PinnedSlot sl;
       sl.dev = dev;
@@ -595,7 +606,10 @@ cudaError_t upload_pinned(const rs_poly_plan &P, void *dst, const void *src, siz
         cudaGetLastError();
       }
     }
-    if (slot) slot->busy = true;
+    if (slot) {
+      slot->busy = true;
+      slot->seq = ++P.stage_seq;
+    }
   }
   if (!slot) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
   std::memcpy(slot->p, src, bytes);

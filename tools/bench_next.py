@@ -5,8 +5,9 @@
   python tools/bench_next.py sweep   [--steps 10]          # erasure-count / (k, m) sweeps (NEXT-2)
 
 Each prints one JSON line per measured case: device time with CUDA events on the launching
-stream (inputs resident in HBM, >> L2), algorithmic bytes, fraction of the measured HBM copy
-peak, and the correctness check that preceded the number (oracle on sampled columns).
+stream (inputs resident in HBM, >> L2; the median of the timed steps, min/median/max listed),
+algorithmic bytes, fraction of the measured HBM copy peak, and the correctness check that
+preceded the number (oracle on sampled columns).
 """
 import argparse
 import json
@@ -99,7 +100,7 @@ def run_update(a):
     total = 1 + a.warmup + a.steps                         # each call toggles old <-> new parity
     bad += sampled_encode_ok(st, new_data if total % 2 else old_data, c, picks)
     moved = S * (2 * len(idx) + 2 * m) * B
-    avg = statistics.mean(ms)
+    avg = statistics.median(ms)
     peak, src = bench.hbm_peak()
     line = {"row": "NEXT-1 diff-update (P:210)", "metric": "changed user data GB/s", "config": a.config,
             "k": k, "m": m, "w": w, "stripes": S, "block_bytes": B, "changed_blocks": idx,
@@ -112,6 +113,7 @@ def run_update(a):
                            f"{S * (k + m) * B / 1e9:.2f} GB vs {moved / 1e9:.2f} GB",
             "verified": {"mismatches": bad, "how": "parity vs oracle re-encode of the new data on sampled "
                                                     "columns of 3 stripes, before and after timing"},
+            "ms_min_med_max": [round(min(ms), 4), round(statistics.median(ms), 4), round(max(ms), 4)],
             "steps": a.steps, "warmup": a.warmup, "clocks": clocks, "jit": plan.stats()["jit_launches"] > 0}
     print(json.dumps(line), flush=True)
     return 0 if bad == 0 else 1
@@ -147,14 +149,21 @@ def sweep_point(k, m, B, S, t, policy, steps, warmup, fig, w=8, poly=0x11D, seed
     bad += 0 if torch.equal(st, golden) else 1
     del golden
     torch.cuda.empty_cache()
-    enc = statistics.mean(timed(lambda: plan.encode_batch(st), steps, warmup, stream))
-    dec = statistics.mean(timed(lambda: plan.decode_batch(st, er), steps, warmup, stream))
+    enc_ms = timed(lambda: plan.encode_batch(st), steps, warmup, stream)
+    dec_ms = timed(lambda: plan.decode_batch(st, er), steps, warmup, stream)
+    # medians: a single slow step (GPU clocks ramping after the host-side oracle check) can
+    # double one sample; min / median / max are all reported
+    enc, dec = statistics.median(enc_ms), statistics.median(dec_ms)
     peak, _ = bench.hbm_peak()
     user = S * k * B
     moved_enc = S * n * B
     moved_dec = S * ((k + t) if (policy == 1 and t < m) else n) * B
     return {"row": "NEXT-2 sweep", "figure": fig, "k": k, "m": m, "w": w, "block_bytes": B, "stripes": S,
             "erasures": t, "read_policy": ["all_survivors", "k_survivors"][policy],
+            "ms_min_med_max": {"encode": [round(min(enc_ms), 4), round(statistics.median(enc_ms), 4),
+                                          round(max(enc_ms), 4)],
+                               "decode": [round(min(dec_ms), 4), round(statistics.median(dec_ms), 4),
+                                          round(max(dec_ms), 4)]},
             "encode": {"gbs_user": round(user / enc / 1e6, 1), "ms": round(enc, 4),
                        "hbm_frac": round(moved_enc / enc / 1e6 / peak, 4)},
             "decode": {"gbs_user": round(user / dec / 1e6, 1), "ms": round(dec, 4),
