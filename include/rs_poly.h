@@ -156,6 +156,19 @@ rs_status rs_poly_update_batch(const rs_poly_plan *plan, void *stripes, size_t n
                                const int *data_idx, int n_changed, const void *old_blocks,
                                size_t old_stripe_stride, size_t old_block_stride, void *stream);
 
+/* ---- the paper's optimisation study (measurement only) ------------
+ * Decodes like rs_poly_decode_batch (one erasure list for every stripe) with a
+ * per-column, table-driven implementation of the two-step decode as the paper describes
+ * HDFS-RAID's code, with its optimisations selected by opt_mask:
+ *   bit 0 Opt1 precomputed alpha powers, bit 1 Opt2 skip erased positions in Step 1,
+ *   bit 2 Opt3 V_E inverted once (else a Gauss-Jordan elimination per column).
+ * opt_mask 0 = "PolyRS" (the HDFS-RAID port), 7 = "OptPolyRS".  Encoding is the same call
+ * with the m parity blocks as the erasures.  Same bytes as the product kernels.
+ * Limits: w = 8, k + m <= 32, 1 <= n_erasures <= min(m, 8); otherwise RS_ERR_INVALID_ARG. */
+rs_status rs_poly_ablation_decode(const rs_poly_plan *plan, void *stripes, size_t n_stripes,
+                                  size_t stripe_stride, size_t block_stride, size_t block_bytes,
+                                  const int *erasures, int n_erasures, int opt_mask, void *stream);
+
 /* ---- run-time specialised kernels (JIT) ----------------------------------------
  * For every erasure pattern E the decode map survivors -> erased symbols is a fixed
  * GF(2)-linear map (R_E = V_E^{-1} A_E, the paper's Step 1 + Step 2 with Opt1/Opt3

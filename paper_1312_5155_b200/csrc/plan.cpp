@@ -1188,6 +1188,45 @@ size_t rs_poly_update_jit_source(const rs_poly_plan *P, const int *data_idx, int
   return s.size();
 }
 
+rs_status rs_poly_ablation_decode(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
+                                  size_t block_stride, size_t block_bytes, const int *erasures, int n_erasures,
+                                  int opt_mask, void *stream) {
+  if (!P || P->w != 8 || P->n > 32 || n_erasures < 1 || n_erasures > std::min(P->m, 8) || !erasures ||
+      opt_mask < 0 || opt_mask > 7)
+    return RS_ERR_INVALID_ARG;
+  rs_status rc = check_strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
+  if (rc) return rc;
+  std::vector<int> er;
+  rc = parse_row(P, erasures, n_erasures, er, false);
+  if (rc) return rc;
+  if (n_stripes == 0) return RS_OK;
+  const Field &F = P->F;
+  const int t = (int)er.size(), n = P->n;
+  // consts: exp[512], log[256], apow[8][32] (alpha^{j*p}, row stride n), vinv[8][8] (row stride t)
+  std::vector<uint8_t> c(768 + 8 * 32 + 8 * 8, 0);
+  for (int i = 0; i < 512; ++i) c[i] = (uint8_t)F.alpha_pow((uint64_t)i);
+  for (int v = 1; v < 256; ++v) c[512 + v] = (uint8_t)F.log_[v];
+  for (int j = 0; j < t; ++j)
+    for (int p = 0; p < n; ++p) c[768 + j * n + p] = (uint8_t)F.alpha_pow((uint64_t)j * (uint64_t)p);
+  std::vector<uint32_t> V((size_t)t * t);
+  for (int j = 0; j < t; ++j)
+    for (int e = 0; e < t; ++e)
+      V[(size_t)j * t + e] = F.alpha_pow((uint64_t)j * (uint64_t)rsb::position(er[e], P->k, P->m));
+  if (!rsb::invert(F, V, t)) return RS_ERR_INVALID_ARG;
+  for (int i = 0; i < t * t; ++i) c[768 + 256 + i] = (uint8_t)V[i];
+  Blob b;
+  const size_t off = b.add(c.data(), c.size());
+  DevBlob d;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = d.upload(*P, b, st);
+  Geometry G = strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
+  if (e == cudaSuccess)
+    e = rsb::launch_polyrs_ablation(G.L, n_stripes, block_bytes, P->k, P->m, er.data(), t, d.p + off, opt_mask,
+                                    sm_count(), st);
+  cudaError_t ef = d.release();
+  return cuda_status(e != cudaSuccess ? e : ef);
+}
+
 rs_status rs_poly_plan_stats(const rs_poly_plan *P, rs_poly_stats *out) {
   if (!P || !out) return RS_ERR_INVALID_ARG;
   std::memset(out, 0, sizeof(*out));

@@ -81,6 +81,11 @@ cudaError_t launch_generic(int w, const GenericArgs &a, cudaStream_t st);
 bool sliced_available(int k, int m, int w, uint32_t poly);
 cudaError_t launch_sliced(int k, int m, int w, uint32_t poly, bool decode, const SlicedArgs &a,
                           cudaStream_t st);
+// The paper's optimisation study (polyrs_ablation.cu): per-column two-step decode with
+// Opt1/Opt2/Opt3 selected by opt_mask bits 0/1/2; GF(2^8), k+m <= 32, 1 <= t <= 8.
+cudaError_t launch_polyrs_ablation(const Layout &L, uint64_t n_stripes, uint64_t block_bytes, int k, int m,
+                                   const int *erased, int t, const uint8_t *dev_consts, int opt_mask,
+                                   int sm_count, cudaStream_t st);
 uint64_t launches_total();
 void count_launch();
 

@@ -47,6 +47,7 @@ _lib.rs_poly_update.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]
 _lib.rs_poly_update_batch.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _i32, _vp, _sz, _sz, _vp]
 _lib.rs_poly_update_jit_source.argtypes = [_vp, _vp, _i32, ctypes.c_char_p, _sz]
 _lib.rs_poly_update_jit_source.restype = _sz
+_lib.rs_poly_ablation_decode.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _i32, _i32, _vp]
 
 
 class Stats(ctypes.Structure):
@@ -255,6 +256,15 @@ class Plan:
         buf = ctypes.create_string_buffer(n + 1)
         _lib.rs_poly_update_jit_source(self._h, ix, len(idx), buf, n + 1)
         return buf.value.decode()
+
+    # ---- the paper's optimisation study (NEXT-3) -----------------------------------
+    def ablation_decode(self, stripes, erasures, opt_mask: int, stream=None) -> None:
+        """Per-column table decode with Opt1/2/3 = opt_mask bits 0/1/2 (0 = PolyRS, 7 = OptPolyRS)."""
+        ptr, S, ss, bs, B = _geometry(stripes, self.n)
+        er = list(erasures)
+        e = (ctypes.c_int * max(1, len(er)))(*er)
+        _check(_lib.rs_poly_ablation_decode(self._h, ptr, S, ss, bs, B, e, len(er), opt_mask, _stream(stream)),
+               "rs_poly_ablation_decode")
 
     # ---- end to end from host memory --------------------------------------------
     def encode_host(self, host_stripes, stream=None):

@@ -200,9 +200,62 @@ def run_sweep(a):
 
 
 # ---------------------------------------------------------------------------------------
+# NEXT-3: the paper's optimisation study on the GPU
+# ---------------------------------------------------------------------------------------
+def run_ablation(a):
+    import torch
+    import paper_1312_5155_b200 as rsp
+    MiB = 1 << 20
+    peak, _ = bench.hbm_peak()
+    bad = 0
+    cases = [(10, 4, t, "decode") for t in (1, 2, 3, 4)] + [(10, m, m, "encode") for m in (2, 4, 6)]
+    for k, m, t, op in cases:
+        n, B = k + m, 4 * MiB
+        S = max(1, (a.data_gib << 30) // (k * B))
+        plan = rsp.Plan(k, m)
+        st = torch.empty((S, n, B), dtype=torch.uint8, device="cuda")
+        rsp.synth_fill(st, k, seed=0)
+        plan.encode_batch(st)
+        golden = st.clone()
+        er = list(range(k, n)) if op == "encode" else synth.erasure_draw(0, 0, range(n), t)
+        er_tab = np.full((S, m), -1, dtype=np.int32)
+        er_tab[:, :t] = er
+        plan.prepare(er_tab)
+        stream = torch.cuda.current_stream()
+        variants = [("PolyRS (no Opt)", 0), ("+Opt1", 1), ("+Opt1+Opt2", 3), ("+Opt3", 4), ("OptPolyRS (Opt1-3)", 7),
+                    ("bit-sliced (product)", None)]
+        res = {}
+        for name, opt in variants:
+            st[:, er] = 0xEE
+            if opt is None:
+                fn = (lambda: plan.encode_batch(st)) if op == "encode" else (lambda: plan.decode_batch(st, er_tab))
+            else:
+                fn = (lambda o=opt: plan.ablation_decode(st, er, o))
+            fn()
+            torch.cuda.synchronize()
+            ok = torch.equal(st, golden)
+            bad += 0 if ok else 1
+            ms = timed(fn, a.steps, 1, stream)
+            med = statistics.median(ms)
+            res[name] = {"ms": round(med, 3), "gbs_user": round(S * k * B / med / 1e6, 1),
+                         "hbm_frac": round(S * n * B / med / 1e6 / peak, 4), "exact": ok}
+        base = res["PolyRS (no Opt)"]["ms"]
+        for v in res.values():
+            v["speedup_vs_PolyRS"] = round(base / v["ms"], 2)
+        line = {"row": "NEXT-3 optimisation study (P:317-327)", "op": op, "k": k, "m": m, "erasures": er,
+                "block_bytes": B, "stripes": S, "variants": res,
+                "paper": "P:440: PolyRS encode >250% of OptPolyRS time at (10,2), ~10% more at (10,6); "
+                         "P:327: Opt1 and Opt3 largest, gains grow with erasures (CPU, qualitative)"}
+        print(json.dumps(line), flush=True)
+        del st, golden
+        torch.cuda.empty_cache()
+    return 0 if bad == 0 else 1
+
+
+# ---------------------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["update", "sweep"])
+    ap.add_argument("what", choices=["update", "sweep", "ablation"])
     ap.add_argument("--data-gib", type=int, default=20, help="sweep: user data per point")
     ap.add_argument("--config", default="C5")
     ap.add_argument("--changed", type=int, default=1)
@@ -213,6 +266,8 @@ def main():
         return run_update(a)
     if a.what == "sweep":
         return run_sweep(a)
+    if a.what == "ablation":
+        return run_ablation(a)
     return 2
 
 
