@@ -156,6 +156,25 @@ rs_status rs_poly_update_batch(const rs_poly_plan *plan, void *stripes, size_t n
                                const int *data_idx, int n_changed, const void *old_blocks,
                                size_t old_stripe_stride, size_t old_block_stride, void *stream);
 
+/* ---- cross-GPU stripe placement ---------------------------------
+ * When the blocks of a stripe live on different GPUs (block b of stripe s
+ * on rank (b + s) mod N), parity = sum_j P[:,j] d_j (linear) splits by
+ * rank: each rank computes the partial parity of the data blocks it holds, and the
+ * owner of each parity block adds (XORs) the partials it receives.
+ * rs_poly_encode_partial, for stripes s = 0..S-1:
+ *   partial[s][i] (^)= sum_q P[i][data_idx[q]] * data[s][q],   i = 0..m-1
+ * data: HOST array [S][c] of DEVICE pointers (block data_idx[q] of stripe s), partial:
+ * HOST array [S][m] of DEVICE pointers; accumulate != 0 XORs into partial, else
+ * overwrites it.  data_idx: c distinct indices in [0,k) (else RS_ERR_BAD_ERASURE); c = 0
+ * writes zero partials (accumulate = 0) or is a no-op.
+ * rs_poly_xor_reduce: dst[s] = srcs[s][0] ^ ... ^ srcs[s][n_src-1] (HOST arrays of DEVICE
+ * pointers, [S] and [S][n_src]; dst may be one of its sources); bytes % (w/8) == 0. */
+rs_status rs_poly_encode_partial(const rs_poly_plan *plan, const int *data_idx, int n_data,
+                                 const void *const *data, void *const *partial, size_t n_stripes,
+                                 size_t block_bytes, int accumulate, void *stream);
+rs_status rs_poly_xor_reduce(const rs_poly_plan *plan, void *const *dst, const void *const *srcs, int n_src,
+                             size_t n_stripes, size_t bytes, void *stream);
+
 /* ---- the paper's optimisation study (measurement only) ------------
  * Decodes like rs_poly_decode_batch (one erasure list for every stripe) with a
  * per-column, table-driven implementation of the two-step decode as the paper describes

@@ -20,6 +20,7 @@
 #include <functional>
 #include <future>
 #include <map>
+#include <string>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -51,14 +52,20 @@ struct PatternHost {
 };
 
 using MaskKey = std::array<uint64_t, 4>;
+// JIT cache key: (kind, mask).  Decode: the erased mask; encode: 0; linear job: its id.
+enum JitKind { kJitDecode = 0, kJitEncode = 1, kJitLinear = 2 };
+using JitKey = std::pair<int, MaskKey>;
 
-// Diff-update of one changed-block set J (sorted): per stripe the kernels see
-// nv = 2c + m virtual blocks, interleaved [new_0, old_0, new_1, old_1, ..., parity_0..m-1],
-// and compute parity_i <- sum_j P[i][j] (new_j + old_j) + parity_i, i.e. M = [P_J P_J | I].
-struct UpdateHost {
-  std::vector<int> idx;     // changed data indices, ascending
-  int nv = 0;
-  std::vector<uint32_t> M;  // m x nv
+// A "linear job": per stripe the kernels see nv virtual blocks (a pointer table) and
+// compute out_r = sum_v M[r][v] in_v for the nout virtual blocks out[r] (which may also
+// be inputs: in place).  Used by the diff-update, the partial encoder of the
+// cross-GPU placement and the XOR reduction.  Cached per plan by a signature string.
+struct LinearHost {
+  int id = 0;               // JIT key
+  int nv = 0, nout = 0;
+  std::vector<int> out;     // virtual indices of the outputs
+  std::vector<uint32_t> M;  // nout x nv
+  int group_blocks = 0;     // JIT CSE group (0 = by field)
   rsb::GenericPat gp{};
   std::vector<uint8_t> tab;
 };
@@ -132,12 +139,12 @@ struct rs_poly_plan {
   std::vector<uint8_t> enc_tab;
   mutable std::mutex mu;
   mutable std::map<MaskKey, std::shared_ptr<const PatternHost>> cache;
-  mutable std::map<MaskKey, std::shared_ptr<const UpdateHost>> upd_cache;  // diff-update sets
+  mutable std::map<std::string, std::shared_ptr<const LinearHost>> lin_cache;  // linear jobs by signature
   // run-time specialised kernels: decode patterns (key = erased mask) and, for codes
   // without a compiled network, the encoder (key = kEncodeKey)
   int jit_mode = RS_JIT_BACKGROUND;
   int read_policy = RS_READ_ALL_SURVIVORS;
-  mutable std::map<MaskKey, std::shared_ptr<JitEntry>> jit;
+  mutable std::map<JitKey, std::shared_ptr<JitEntry>> jit;
   std::vector<std::shared_ptr<JitEntry>> retired;  // dropped by a policy change, released at destroy
   mutable std::map<int, std::vector<cudaStream_t>> pool;  // device -> side streams for concurrent launches
   mutable std::atomic<uint64_t> jit_launches{0}, table_launches{0};
@@ -336,7 +343,7 @@ struct Geometry {
 
 bool ptr_aligned(uint64_t v, uint64_t a) { return (v % a) == 0; }
 
-const MaskKey kEncodeKey{~0ull, ~0ull, ~0ull, ~0ull};
+const JitKey kEncodeKey{kJitEncode, MaskKey{0, 0, 0, 0}};
 
 bool jit_eligible(const rs_poly_plan &P, int n_out) { return P.w == 8 ? n_out <= 8 : n_out <= 4; }
 
@@ -408,7 +415,7 @@ rsb::jit::Spec decoder_spec(const rs_poly_plan &P, const PatternHost &ph) {
 
 // The compiled kernel for `key` if it is ready; schedules (background) or runs (sync /
 // wait) its compilation on first request.  Must be called without holding P.mu.
-const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const MaskKey &key, const std::function<rsb::jit::Spec()> &mk,
+const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const JitKey &key, const std::function<rsb::jit::Spec()> &mk,
                                 bool wait) {
   if (P.jit_mode == RS_JIT_OFF || !rsb::jit::available()) return nullptr;
   std::shared_ptr<JitEntry> e;
@@ -713,56 +720,91 @@ rs_status collect_patterns(const rs_poly_plan *P, const std::vector<std::vector<
   return RS_OK;
 }
 
-// ---- diff-update ----------------------------------------------------
-MaskKey update_key(const std::vector<int> &idx) {
-  MaskKey key{0, 0, 0, 1ull << 63};  // bit 255 is never an API block (n <= 255): tags the update space
-  for (int j : idx) key[j >> 6] |= 1ull << (j & 63);
-  return key;
-}
-
-std::shared_ptr<const UpdateHost> update_host(const rs_poly_plan &P, const std::vector<int> &idx) {
-  const MaskKey key = update_key(idx);
+// ---- linear jobs (diff-update, partial encode, XOR reduction) ----------------
+// Cached LinearHost for `sig`, built by `fill` (which sets nv, out, M, group_blocks).
+std::shared_ptr<const LinearHost> linear_host(const rs_poly_plan &P, const std::string &sig,
+                                              const std::function<void(LinearHost &)> &fill) {
   std::lock_guard<std::mutex> lock(P.mu);
-  auto it = P.upd_cache.find(key);
-  if (it != P.upd_cache.end()) return it->second;
-  auto uh = std::make_shared<UpdateHost>();
-  const int c = (int)idx.size(), m = P.m, k = P.k;
-  uh->idx = idx;
-  uh->nv = 2 * c + m;
-  uh->M.assign((size_t)m * uh->nv, 0);
-  for (int i = 0; i < m; ++i) {
-    for (int q = 0; q < c; ++q) {
-      const uint32_t coef = P.pmap[(size_t)i * k + idx[q]];  // x^{m+j} mod g, coefficient of x^i
-      uh->M[(size_t)i * uh->nv + 2 * q] = coef;      // new_j
-      uh->M[(size_t)i * uh->nv + 2 * q + 1] = coef;  // old_j (char 2: + = -)
-    }
-    uh->M[(size_t)i * uh->nv + 2 * c + i] = 1;       // the old parity itself
-  }
-  std::memset(&uh->gp, 0, sizeof(uh->gp));
-  uh->gp.n_in = uh->nv;
-  uh->gp.n_out = m;
-  for (int v = 0; v < uh->nv; ++v) uh->gp.in_blk[v] = (uint8_t)v;
-  for (int i = 0; i < m; ++i) uh->gp.out_blk[i] = (uint8_t)(2 * c + i);
-  pack_generic_tables(P.F, P.w, uh->M, m, uh->nv, uh->tab);
-  P.upd_cache.emplace(key, uh);
-  return uh;
+  auto it = P.lin_cache.find(sig);
+  if (it != P.lin_cache.end()) return it->second;
+  auto lh = std::make_shared<LinearHost>();
+  fill(*lh);
+  lh->id = (int)P.lin_cache.size() + 1;
+  lh->nout = (int)lh->out.size();
+  std::memset(&lh->gp, 0, sizeof(lh->gp));
+  lh->gp.n_in = lh->nv;
+  lh->gp.n_out = lh->nout;
+  for (int v = 0; v < lh->nv; ++v) lh->gp.in_blk[v] = (uint8_t)v;
+  for (int r = 0; r < lh->nout; ++r) lh->gp.out_blk[r] = (uint8_t)lh->out[r];
+  pack_generic_tables(P.F, P.w, lh->M, lh->nout, lh->nv, lh->tab);
+  P.lin_cache.emplace(sig, lh);
+  return lh;
 }
 
-rsb::jit::Spec update_spec(const rs_poly_plan &P, const UpdateHost &uh) {
-  std::vector<int> in(uh.nv), out(P.m);
-  for (int v = 0; v < uh.nv; ++v) in[v] = v;
-  for (int i = 0; i < P.m; ++i) out[i] = 2 * (int)uh.idx.size() + i;
-  rsb::jit::Spec s = jit_spec(P, in, out, uh.M);
-  s.group_blocks = P.w == 8 ? 12 : 4;  // even: each (new_j, old_j) pair shares a CSE group
+rsb::jit::Spec linear_spec(const rs_poly_plan &P, const LinearHost &lh) {
+  std::vector<int> in(lh.nv);
+  for (int v = 0; v < lh.nv; ++v) in[v] = v;
+  rsb::jit::Spec s = jit_spec(P, in, lh.out, lh.M);
+  if (lh.group_blocks) s.group_blocks = lh.group_blocks;
   return s;
 }
 
-// ptrs: host [S][nv] virtual block addresses.  Parity is updated in place.
-rs_status update_impl(const rs_poly_plan *P, const UpdateHost &uh, const std::vector<uint64_t> &ptrs,
+// Diff-update of the sorted changed set idx: virtual blocks [new_0, old_0, new_1, old_1, ...,
+// parity_0..m-1]; parity_i <- sum_j P[i][j] (new_j + old_j) + parity_i, M = [P_J P_J | I].
+std::shared_ptr<const LinearHost> update_host(const rs_poly_plan &P, const std::vector<int> &idx) {
+  std::string sig = "U";
+  for (int j : idx) sig += ":" + std::to_string(j);
+  return linear_host(P, sig, [&](LinearHost &lh) {
+    const int c = (int)idx.size(), m = P.m, k = P.k;
+    lh.nv = 2 * c + m;
+    for (int i = 0; i < m; ++i) lh.out.push_back(2 * c + i);
+    lh.M.assign((size_t)m * lh.nv, 0);
+    for (int i = 0; i < m; ++i) {
+      for (int q = 0; q < c; ++q) {
+        const uint32_t coef = P.pmap[(size_t)i * k + idx[q]];  // x^{m+j} mod g, coefficient of x^i
+        lh.M[(size_t)i * lh.nv + 2 * q] = coef;      // new_j
+        lh.M[(size_t)i * lh.nv + 2 * q + 1] = coef;  // old_j (char 2: + = -)
+      }
+      lh.M[(size_t)i * lh.nv + 2 * c + i] = 1;       // the old parity itself
+    }
+    lh.group_blocks = P.w == 8 ? 12 : 4;  // even: each (new_j, old_j) pair shares a CSE group
+  });
+}
+
+// Partial parity of the data subset idx (cross-GPU placement): virtual blocks
+// [d_0..d_{c-1}, partial_0..partial_{m-1}]; partial_i <- sum_j P[i][j] d_j (+ partial_i).
+std::shared_ptr<const LinearHost> partial_host(const rs_poly_plan &P, const std::vector<int> &idx, bool acc) {
+  std::string sig = acc ? "PA" : "P";
+  for (int j : idx) sig += ":" + std::to_string(j);
+  return linear_host(P, sig, [&](LinearHost &lh) {
+    const int c = (int)idx.size(), m = P.m, k = P.k;
+    lh.nv = c + m;
+    for (int i = 0; i < m; ++i) lh.out.push_back(c + i);
+    lh.M.assign((size_t)m * lh.nv, 0);
+    for (int i = 0; i < m; ++i) {
+      for (int q = 0; q < c; ++q) lh.M[(size_t)i * lh.nv + q] = P.pmap[(size_t)i * k + idx[q]];
+      if (acc) lh.M[(size_t)i * lh.nv + c + i] = 1;
+    }
+    lh.group_blocks = P.w == 8 ? 12 : 3;
+  });
+}
+
+// XOR of n_src blocks into one: virtual blocks [src_0..src_{n-1}, dst]; dst <- sum src.
+std::shared_ptr<const LinearHost> xor_host(const rs_poly_plan &P, int n_src) {
+  return linear_host(P, "X:" + std::to_string(n_src), [&](LinearHost &lh) {
+    lh.nv = n_src + 1;
+    lh.out.push_back(n_src);
+    lh.M.assign((size_t)lh.nv, 0);
+    for (int q = 0; q < n_src; ++q) lh.M[q] = 1;  // all pass-through: raw XOR, no transposes
+  });
+}
+
+// ptrs: host [S][nv] virtual block addresses.
+rs_status linear_impl(const rs_poly_plan *P, const LinearHost &lh, const std::vector<uint64_t> &ptrs,
                       size_t n_stripes, size_t B, cudaStream_t st) {
   Geometry G;
   G.L.base = nullptr;
-  G.L.n = uh.nv;
+  G.L.n = lh.nv;
   G.n_stripes = n_stripes;
   G.block_bytes = B;
   G.aligned32 = G.aligned16 = true;
@@ -772,15 +814,16 @@ rs_status update_impl(const rs_poly_plan *P, const UpdateHost &uh, const std::ve
   }
   uint64_t body = body_units_of(*P, G);
   const rsb::jit::Kernel *jk = nullptr;
-  if (body && jit_eligible(*P, P->m))
-    jk = jit_get(*P, update_key(uh.idx), [&] { return update_spec(*P, uh); }, false);
+  if (body && jit_eligible(*P, lh.nout))
+    jk = jit_get(*P, JitKey{kJitLinear, MaskKey{(uint64_t)lh.id, 0, 0, 0}}, [&] { return linear_spec(*P, lh); },
+                 false);
   if (!jk) body = 0;
   Blob b;
   const size_t ptrs_off = b.add(ptrs.data(), sizeof(uint64_t) * ptrs.size());
-  rsb::GenericPat gp = uh.gp;
+  rsb::GenericPat gp = lh.gp;
   gp.table_off = 0;
   const size_t pats_off = b.add(&gp, sizeof(gp));
-  const size_t tables_off = b.add(uh.tab.data(), uh.tab.size());
+  const size_t tables_off = b.add(lh.tab.data(), lh.tab.size());
   DevBlob d;
   cudaError_t e = d.upload(*P, b, st);
   if (e == cudaSuccess) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
@@ -791,7 +834,7 @@ rs_status update_impl(const rs_poly_plan *P, const UpdateHost &uh, const std::ve
   const uint64_t UB = 32ull * (uint64_t)P->w / 8;
   if (e == cudaSuccess)
     e = launch_generic_range(*P, G, body * UB, G.block_bytes, d.p, pats_off, SIZE_MAX, tables_off,
-                             (uint32_t)((P->m + 3) / 4), (uint32_t)(uh.nv * (P->w == 8 ? 128 : 512)), st);
+                             (uint32_t)((lh.nout + 3) / 4), (uint32_t)(lh.nv * (P->w == 8 ? 128 : 512)), st);
   cudaError_t ef = d.release();
   return cuda_status(e != cudaSuccess ? e : ef);
 }
@@ -818,7 +861,7 @@ rs_status parse_update(const rs_poly_plan *P, const int *data_idx, int c, std::v
 
 const rsb::jit::Kernel *pattern_jit(const rs_poly_plan &P, const PatternHost &ph, const MaskKey &key, bool wait) {
   if (!jit_eligible(P, (int)ph.erased.size())) return nullptr;
-  return jit_get(P, key, [&] { return decoder_spec(P, ph); }, wait);
+  return jit_get(P, JitKey{kJitDecode, key}, [&] { return decoder_spec(P, ph); }, wait);
 }
 
 // rows: per stripe list of erased API indices (validated, sorted ascending)
@@ -1052,7 +1095,7 @@ rs_status rs_poly_plan_set_read_policy(rs_poly_plan *P, int policy) {
   P->read_policy = policy;
   P->cache.clear();
   for (auto it = P->jit.begin(); it != P->jit.end();) {
-    if ((it->first[3] >> 63) == 0) {  // erasure-pattern kernels (encode/update keys carry bit 255)
+    if (it->first.first == kJitDecode) {  // erasure-pattern kernels depend on the policy
       P->retired.push_back(it->second);
       it = P->jit.erase(it);
     } else {
@@ -1139,7 +1182,7 @@ rs_status rs_poly_update(const rs_poly_plan *P, const int *data_idx, int n_chang
     if (!v) return RS_ERR_INVALID_ARG;
     else if (v % a) return RS_ERR_GEOMETRY;
   auto uh = update_host(*P, idx);
-  return update_impl(P, *uh, ptrs, 1, block_bytes, static_cast<cudaStream_t>(stream));
+  return linear_impl(P, *uh, ptrs, 1, block_bytes, static_cast<cudaStream_t>(stream));
 }
 
 rs_status rs_poly_update_batch(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
@@ -1171,7 +1214,53 @@ rs_status rs_poly_update_batch(const rs_poly_plan *P, void *stripes, size_t n_st
     }
     for (int i = 0; i < P->m; ++i) ptrs.push_back(base + s * stripe_stride + (uint64_t)(P->k + i) * block_stride);
   }
-  return update_impl(P, *uh, ptrs, n_stripes, block_bytes, static_cast<cudaStream_t>(stream));
+  return linear_impl(P, *uh, ptrs, n_stripes, block_bytes, static_cast<cudaStream_t>(stream));
+}
+
+rs_status rs_poly_encode_partial(const rs_poly_plan *P, const int *data_idx, int n_data, const void *const *data,
+                                 void *const *partial, size_t n_stripes, size_t block_bytes, int accumulate,
+                                 void *stream) {
+  if (!P) return RS_ERR_INVALID_ARG;
+  std::vector<int> idx, order;
+  rs_status rc = parse_update(P, data_idx, n_data, idx, order);
+  if (rc) return rc;
+  rc = check_geometry(P, block_bytes);
+  if (rc) return rc;
+  if (n_stripes == 0 || (n_data == 0 && accumulate)) return RS_OK;
+  if (!partial || (n_data && !data)) return RS_ERR_INVALID_ARG;
+  const uint64_t a = (uint64_t)(P->w / 8);
+  auto lh = partial_host(*P, idx, accumulate != 0);
+  std::vector<uint64_t> ptrs;
+  ptrs.reserve(n_stripes * (size_t)lh->nv);
+  for (size_t s = 0; s < n_stripes; ++s) {
+    for (int q : order) ptrs.push_back(reinterpret_cast<uint64_t>(data[s * (size_t)n_data + q]));
+    for (int i = 0; i < P->m; ++i) ptrs.push_back(reinterpret_cast<uint64_t>(partial[s * (size_t)P->m + i]));
+  }
+  for (uint64_t v : ptrs)
+    if (!v) return RS_ERR_INVALID_ARG;
+    else if (v % a) return RS_ERR_GEOMETRY;
+  return linear_impl(P, *lh, ptrs, n_stripes, block_bytes, static_cast<cudaStream_t>(stream));
+}
+
+rs_status rs_poly_xor_reduce(const rs_poly_plan *P, void *const *dst, const void *const *srcs, int n_src,
+                             size_t n_stripes, size_t bytes, void *stream) {
+  if (!P || n_src < 1 || n_src + 1 > RS_POLY_MAX_N) return RS_ERR_INVALID_ARG;
+  rs_status rc = check_geometry(P, bytes);
+  if (rc) return rc;
+  if (n_stripes == 0) return RS_OK;
+  if (!dst || !srcs) return RS_ERR_INVALID_ARG;
+  const uint64_t a = (uint64_t)(P->w / 8);
+  auto lh = xor_host(*P, n_src);
+  std::vector<uint64_t> ptrs;
+  ptrs.reserve(n_stripes * (size_t)lh->nv);
+  for (size_t s = 0; s < n_stripes; ++s) {
+    for (int q = 0; q < n_src; ++q) ptrs.push_back(reinterpret_cast<uint64_t>(srcs[s * (size_t)n_src + q]));
+    ptrs.push_back(reinterpret_cast<uint64_t>(dst[s]));
+  }
+  for (uint64_t v : ptrs)
+    if (!v) return RS_ERR_INVALID_ARG;
+    else if (v % a) return RS_ERR_GEOMETRY;
+  return linear_impl(P, *lh, ptrs, n_stripes, bytes, static_cast<cudaStream_t>(stream));
 }
 
 size_t rs_poly_update_jit_source(const rs_poly_plan *P, const int *data_idx, int n_changed, char *buf,
@@ -1179,7 +1268,7 @@ size_t rs_poly_update_jit_source(const rs_poly_plan *P, const int *data_idx, int
   if (!P || n_changed < 1 || !jit_eligible(*P, P->m)) return 0;
   std::vector<int> idx, order;
   if (parse_update(P, data_idx, n_changed, idx, order)) return 0;
-  const std::string s = rsb::jit::source(P->F, update_spec(*P, *update_host(*P, idx)), nullptr);
+  const std::string s = rsb::jit::source(P->F, linear_spec(*P, *update_host(*P, idx)), nullptr);
   if (buf && cap) {
     const size_t nc = std::min(cap - 1, s.size());
     std::memcpy(buf, s.data(), nc);

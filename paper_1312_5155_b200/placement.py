@@ -1,0 +1,124 @@
+"""Cross-GPU stripe placement: encode when a stripe's blocks live on different GPUs.
+
+In a distributed store (the HDFS-RAID setting that motivates the paper) the n
+blocks of a stripe sit on different nodes.  Here block b of stripe s lives on rank
+``(b + s) % world`` (the rotation spreads parity ownership).  Because the code is linear
+ and parity = sum_j P[:, j] d_j (the parity map of g), encoding splits into
+
+1. **local partial parity**: every rank computes, for each stripe, the m partial parities of
+   the data blocks it holds (``rs_poly_encode_partial``; the partial of a parity block the
+   rank itself owns is written straight into that block);
+2. **exchange**: each partial goes to the owner of its parity block, one ``all_to_all``
+   over the process group (NCCL over NVLink/NVSwitch on GPUs);
+3. **XOR reduction**: each owner adds (XORs, GF(2^w) addition) the partials it received into
+   its parity block (``rs_poly_xor_reduce``).
+
+The result equals rs_poly_encode of the whole stripe (tests/test_dist_placement.py checks it
+against the oracle with gloo ranks; tests/test_gpu_placement.py runs the GPU kernels with
+in-process ranks).  The byte traffic and the alternatives are discussed in DESIGN.md §8.
+
+``ops`` supplies the compute steps; the default is the CUDA library (``Plan``).  Tests of the
+host-side protocol inject CPU implementations -- the product path itself has no CPU fallback.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+def owner(block: int, stripe: int, world: int) -> int:
+    """Rank holding API block `block` of stripe `stripe`."""
+    return (block + stripe) % world
+
+
+@dataclass
+class Layout:
+    k: int
+    m: int
+    world: int
+
+    @property
+    def n(self) -> int:
+        return self.k + self.m
+
+    def data_on(self, rank: int, s: int) -> list[int]:
+        return [j for j in range(self.k) if owner(j, s, self.world) == rank]
+
+    def parity_owner(self, i: int, s: int) -> int:
+        return owner(self.k + i, s, self.world)
+
+    def blocks_on(self, rank: int, s: int) -> list[int]:
+        return [b for b in range(self.n) if owner(b, s, self.world) == rank]
+
+    def sends(self, src: int, dst: int, S: int) -> list[tuple[int, int]]:
+        """(stripe, parity index) partials rank `src` sends to rank `dst`, in wire order."""
+        if src == dst:
+            return []
+        return [(s, i) for s in range(S) for i in range(self.m)
+                if self.parity_owner(i, s) == dst and self.data_on(src, s)]
+
+
+class CudaOps:
+    """Compute steps on the GPU through the C ABI (the product path)."""
+
+    def __init__(self, plan):
+        self.plan = plan
+
+    def encode_partial(self, idx, data, partial, nbytes):
+        self.plan.encode_partial(idx, data, partial, nbytes, accumulate=False)
+
+    def xor_reduce(self, dst, srcs, nbytes):
+        self.plan.xor_reduce(dst, srcs, nbytes)
+
+    def empty(self, nblocks, nbytes, like):
+        import torch
+        return torch.empty((nblocks, nbytes), dtype=torch.uint8, device=like.device)
+
+
+def encode_distributed(lay: Layout, store: dict, S: int, nbytes: int, rank: int, all_to_all, ops) -> dict:
+    """SPMD: run on every rank.  `store[(s, b)]` holds this rank's blocks (uint8 [nbytes]
+    tensors; its parity blocks are overwritten).  `all_to_all(send, in_splits, out_splits)`
+    moves a [rows, nbytes] buffer between ranks (rows per destination / source) and returns
+    the received [rows, nbytes] buffer.  Returns counters for the caller's report."""
+    k, m, N = lay.k, lay.m, lay.world
+    like = next(iter(store.values()))
+    # wire order of the send buffer: by destination rank, then (stripe, parity index)
+    send_rows = {d: lay.sends(rank, d, S) for d in range(N)}
+    row_of = {}
+    for d in range(N):
+        for si in send_rows[d]:
+            row_of[si] = len(row_of)
+    send = ops.empty(max(1, len(row_of)), nbytes, like)
+    junk = ops.empty(1, nbytes, like)[0]  # target of partials nobody needs (rank without data in s)
+    # 1. partial parities, batched by the set of local data blocks (N distinct sets under rotation)
+    groups: dict[tuple, list[int]] = {}
+    for s in range(S):
+        groups.setdefault(tuple(lay.data_on(rank, s)), []).append(s)
+    for idx, stripes in groups.items():
+        data = [[store[(s, j)] for j in idx] for s in stripes]
+        # owned parity blocks take this rank's partial directly; a rank without data in a
+        # stripe writes zeros there (c = 0) and sends nothing
+        partial = [[store[(s, k + i)] if lay.parity_owner(i, s) == rank
+                    else (send[row_of[(s, i)]] if (s, i) in row_of else junk)
+                    for i in range(m)] for s in stripes]
+        ops.encode_partial(list(idx), data, partial, nbytes)
+    # 2. exchange
+    in_splits = [len(send_rows[d]) for d in range(N)]
+    recv_rows = {r: lay.sends(r, rank, S) for r in range(N)}
+    out_splits = [len(recv_rows[r]) for r in range(N)]
+    recv = all_to_all(send[:sum(in_splits)], in_splits, out_splits)
+    # 3. XOR the received partials into the owned parity blocks, batched by source count
+    got: dict[tuple[int, int], list] = {}
+    row = 0
+    for r in range(N):
+        for si in recv_rows[r]:
+            got.setdefault(si, []).append(recv[row])
+            row += 1
+    by_n: dict[int, list] = {}
+    for (s, i), parts in got.items():
+        by_n.setdefault(len(parts), []).append((s, i, parts))
+    for nsrc, items in by_n.items():
+        dst = [store[(s, k + i)] for s, i, _ in items]
+        srcs = [[store[(s, k + i)]] + parts for s, i, parts in items]
+        ops.xor_reduce(dst, srcs, nbytes)
+    return {"sent_blocks": sum(in_splits), "received_blocks": sum(out_splits),
+            "local_partial_calls": len(groups), "xor_calls": len(by_n)}

@@ -48,6 +48,8 @@ _lib.rs_poly_update_batch.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _i32, _
 _lib.rs_poly_update_jit_source.argtypes = [_vp, _vp, _i32, ctypes.c_char_p, _sz]
 _lib.rs_poly_update_jit_source.restype = _sz
 _lib.rs_poly_ablation_decode.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _i32, _i32, _vp]
+_lib.rs_poly_encode_partial.argtypes = [_vp, _vp, _i32, _vp, _vp, _sz, _sz, _i32, _vp]
+_lib.rs_poly_xor_reduce.argtypes = [_vp, _vp, _vp, _i32, _sz, _sz, _vp]
 
 
 class Stats(ctypes.Structure):
@@ -256,6 +258,25 @@ class Plan:
         buf = ctypes.create_string_buffer(n + 1)
         _lib.rs_poly_update_jit_source(self._h, ix, len(idx), buf, n + 1)
         return buf.value.decode()
+
+    # ---- cross-GPU placement pieces (NEXT-4) ----------------------------------------
+    def encode_partial(self, data_idx, data, partial, block_bytes: int, accumulate: bool = False,
+                       stream=None) -> None:
+        """partial[s][i] (^)= sum_q P[i][data_idx[q]] data[s][q]; data [S][c], partial [S][m] (pointers/tensors)."""
+        idx = list(data_idx)
+        c, S = len(idx), len(partial)
+        ix = (ctypes.c_int * max(1, c))(*idx)
+        d = (ctypes.c_void_p * max(1, S * c))(*[_ptr(x) for row in data for x in row])
+        p = (ctypes.c_void_p * (S * self.m))(*[_ptr(x) for row in partial for x in row])
+        _check(_lib.rs_poly_encode_partial(self._h, ix, c, d, p, S, block_bytes, int(accumulate), _stream(stream)),
+               "rs_poly_encode_partial")
+
+    def xor_reduce(self, dst, srcs, nbytes: int, stream=None) -> None:
+        """dst[s] = XOR of srcs[s][*] (lists of pointers/tensors; dst may alias a source)."""
+        S, n_src = len(dst), len(srcs[0])
+        dp = (ctypes.c_void_p * S)(*[_ptr(x) for x in dst])
+        sp = (ctypes.c_void_p * (S * n_src))(*[_ptr(x) for row in srcs for x in row])
+        _check(_lib.rs_poly_xor_reduce(self._h, dp, sp, n_src, S, nbytes, _stream(stream)), "rs_poly_xor_reduce")
 
     # ---- the paper's optimisation study (NEXT-3) -----------------------------------
     def ablation_decode(self, stripes, erasures, opt_mask: int, stream=None) -> None:

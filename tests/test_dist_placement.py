@@ -1,0 +1,98 @@
+"""Cross-GPU stripe placement (NEXT-4): the host-side protocol with gloo ranks on CPU.
+
+paper_1312_5155_b200/placement.py runs SPMD: local partial parities, an all_to_all of the
+partials to the parity owners, XOR reduction.  Here the compute steps are CPU stand-ins
+built from the oracle (test infrastructure; the product uses the CUDA kernels, checked in
+tests/test_gpu_placement.py), so what is tested is the placement, the wire order and the
+reduction bookkeeping: every owner's parity must equal the oracle's encoding of the stripe.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+
+P8 = 0x11D
+
+
+class OracleOps:
+    """CPU stand-ins: partial = oracle encoding of the stripe with only blocks idx non-zero."""
+
+    def __init__(self, k, m):
+        self.k, self.m = k, m
+
+    def encode_partial(self, idx, data, partial, nbytes):
+        for drow, prow in zip(data, partial):
+            st = np.zeros((1, self.k + self.m, nbytes), dtype=np.uint8)
+            for j, d in zip(idx, drow):
+                st[0, j] = d.numpy()
+            oracle.encode_bulk(st, self.k, self.m, 8, P8)
+            for i in range(self.m):
+                prow[i].copy_(torch.from_numpy(st[0, self.k + i].copy()))
+
+    def xor_reduce(self, dst, srcs, nbytes):
+        for d, row in zip(dst, srcs):
+            acc = np.zeros(nbytes, dtype=np.uint8)
+            for x in row:
+                acc ^= x.numpy()
+            d.copy_(torch.from_numpy(acc))
+
+    def empty(self, nblocks, nbytes, like):
+        return torch.empty((nblocks, nbytes), dtype=torch.uint8)
+
+
+def _worker(rank, world, k, m, S, B, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1312_5155_b200.placement import Layout, encode_distributed
+    lay = Layout(k, m, world)
+    full = synth.stripes_array(3, range(S), k, m, B)
+    store = {}
+    for s in range(S):
+        for b in lay.blocks_on(rank, s):
+            store[(s, b)] = torch.from_numpy(full[s, b].copy()) if b < k else torch.full((B,), 0xCD, dtype=torch.uint8)
+
+    def a2a(send, in_splits, out_splits):
+        out = torch.empty((sum(out_splits), B), dtype=torch.uint8)
+        dist.all_to_all_single(out.view(-1), send.reshape(-1).contiguous(),
+                               [x * B for x in out_splits], [x * B for x in in_splits])
+        return out
+
+    stats = encode_distributed(lay, store, S, B, rank, a2a, OracleOps(k, m))
+    ref = full.copy()
+    oracle.encode_bulk(ref, k, m, 8, P8)
+    bad = 0
+    for (s, b), t in store.items():
+        bad += int(not np.array_equal(t.numpy(), ref[s, b]))
+    q.put((rank, bad, stats))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,m", [(2, 10, 4), (3, 6, 3), (4, 2, 2)])
+def test_placement_protocol_gloo(world, k, m):
+    S, B = 7, 96
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + world * 7 + k
+    ps = [ctx.Process(target=_worker, args=(r, world, k, m, S, B, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(bad == 0 for _, bad, _ in res), res
+    assert sum(st["sent_blocks"] for _, _, st in res) == sum(st["received_blocks"] for _, _, st in res)
+
+
+def test_layout_owner_rotation():
+    from paper_1312_5155_b200.placement import Layout
+    lay = Layout(10, 4, 8)
+    for s in range(8):
+        assert sorted(b for r in range(8) for b in lay.blocks_on(r, s)) == list(range(14))
+    owners = [lay.parity_owner(i, s) for s in range(8) for i in range(4)]
+    assert sorted(set(owners)) == list(range(8))          # rotation spreads parity ownership
