@@ -253,9 +253,76 @@ def run_ablation(a):
 
 
 # ---------------------------------------------------------------------------------------
+# NEXT-4: cross-GPU placement -- one rank's compute at C5 scale (the exchange needs N GPUs)
+# ---------------------------------------------------------------------------------------
+def run_placement(a):
+    import torch
+    import paper_1312_5155_b200 as rsp
+    from paper_1312_5155_b200.placement import Layout
+    c = synth.CONFIGS["C5"]
+    k, m, B, S, N = c["k"], c["m"], c["block_bytes"], c["stripes"], a.world
+    lay = Layout(k, m, N)
+    rank = 0
+    plan = rsp.Plan(k, m)
+    plan.set_jit(rsp.RS_JIT_SYNC)
+    peak, _ = bench.hbm_peak()
+    groups = {}
+    for s in range(S):
+        groups.setdefault(tuple(lay.data_on(rank, s)), []).append(s)
+    nloc = sum(len(idx) * len(st) for idx, st in groups.items())
+    data = torch.randint(0, 256, (max(1, nloc), B), dtype=torch.uint8, device="cuda")
+    parts = torch.empty((S * m, B), dtype=torch.uint8, device="cuda")
+    calls, row = [], 0
+    for idx, stripes in groups.items():
+        d = [[data[row + q * len(stripes) + si] for q in range(len(idx))] for si in range(len(stripes))]
+        p = [[parts[s * m + i] for i in range(m)] for s in stripes]
+        row += len(idx) * len(stripes)
+        calls.append((list(idx), d, p))
+    owned = [(s, i) for s in range(S) for i in range(m) if lay.parity_owner(i, s) == rank]
+    nsrc = [1 + sum(1 for r in range(N) if r != rank and lay.data_on(r, s)) for s, i in owned]
+    recv = torch.randint(0, 256, (sum(nsrc) - len(owned), B), dtype=torch.uint8, device="cuda")
+    par = torch.empty((len(owned), B), dtype=torch.uint8, device="cuda")
+    by_n = {}
+    r0 = 0
+    for o, (si, ns) in enumerate(zip(owned, nsrc)):
+        by_n.setdefault(ns, ([], []))
+        by_n[ns][0].append(par[o])
+        by_n[ns][1].append([par[o]] + [recv[r0 + q] for q in range(ns - 1)])
+        r0 += ns - 1
+
+    def partial_step():
+        for idx, d, p in calls:
+            plan.encode_partial(idx, d, p, B)
+
+    def xor_step():
+        for dst, srcs in by_n.values():
+            plan.xor_reduce(dst, srcs, B)
+
+    stream = torch.cuda.current_stream()
+    ms_p = statistics.median(timed(partial_step, a.steps, a.warmup, stream))
+    ms_x = statistics.median(timed(xor_step, a.steps, a.warmup, stream))
+    bytes_p = (nloc + S * m) * B
+    bytes_x = (sum(nsrc) + len(owned)) * B
+    nvlink = sum(len(lay.sends(r, d, S)) for r in range(N) for d in range(N)) * B
+    line = {"row": "NEXT-4 cross-GPU placement (one rank's compute)", "world": N, "rank": rank, "k": k, "m": m,
+            "stripes": S, "block_bytes": B,
+            "partial_encode": {"ms": round(ms_p, 4), "bytes": bytes_p,
+                               "hbm_frac": round(bytes_p / ms_p / 1e6 / peak, 4), "local_data_blocks": nloc},
+            "xor_reduce": {"ms": round(ms_x, 4), "bytes": bytes_x, "hbm_frac": round(bytes_x / ms_x / 1e6 / peak, 4),
+                           "owned_parity_blocks": len(owned)},
+            "exchange": {"partials_over_nvlink_all_ranks_bytes": nvlink,
+                         "gather_alternative_bytes": sum(k - len(lay.data_on(lay.parity_owner(0, s), s)) + m - 1
+                                                         for s in range(S)) * B,
+                         "measured": False, "why": "one GPU per gpurun call; the exchange is an NCCL all_to_all"}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["update", "sweep", "ablation"])
+    ap.add_argument("what", choices=["update", "sweep", "ablation", "placement"])
+    ap.add_argument("--world", type=int, default=8, help="placement: ranks of the emulated layout")
     ap.add_argument("--data-gib", type=int, default=20, help="sweep: user data per point")
     ap.add_argument("--config", default="C5")
     ap.add_argument("--changed", type=int, default=1)
@@ -268,6 +335,8 @@ def main():
         return run_sweep(a)
     if a.what == "ablation":
         return run_ablation(a)
+    if a.what == "placement":
+        return run_placement(a)
     return 2
 
 
