@@ -344,6 +344,9 @@ struct Geometry {
 bool ptr_aligned(uint64_t v, uint64_t a) { return (v % a) == 0; }
 
 const JitKey kEncodeKey{kJitEncode, MaskKey{0, 0, 0, 0}};
+// At most this many JIT modules per plan (each is ~50-150 KB of code); RS(10,4) has 1001
+// erasure patterns, RS(12,4) 2516.  Beyond it, new patterns run on the table kernels.
+constexpr size_t kMaxJitKernels = 8192;
 
 bool jit_eligible(const rs_poly_plan &P, int n_out) { return P.w == 8 ? n_out <= 8 : n_out <= 4; }
 
@@ -425,6 +428,8 @@ const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const JitKey &key, const 
     auto it = P.jit.find(key);
     if (it != P.jit.end()) {
       e = it->second;
+    } else if (P.jit.size() >= kMaxJitKernels) {
+      return nullptr;  // bounded module count per plan: further patterns use the table kernels
     } else {
       e = std::make_shared<JitEntry>();
       prom = std::make_shared<std::promise<std::shared_ptr<rsb::jit::Kernel>>>();

@@ -144,3 +144,46 @@ def test_k_survivor_read_policy(k, m, w, poly, B, jit):
         for b in er[s]:
             if b >= 0:
                 assert np.array_equal(got[s, b], ref[s, b]), (s, b)
+
+
+def test_concurrent_host_threads_share_a_plan():
+    """One plan used from 4 host threads at once (own streams, different batches and patterns,
+    background JIT compiling while calls run): every result exact."""
+    import threading
+    k, m, B, S = 10, 4, 64 * 1024, 6
+    m_ = rs()
+    plan = m_.Plan(k, m)
+    refs = [encoded(k, m, 8, P8, B, S, seed=50 + t) for t in range(4)]
+    errs = []
+
+    def worker(t):
+        try:
+            stream = torch.cuda.Stream()
+            rng = np.random.default_rng(t)
+            with torch.cuda.stream(stream):
+                for it in range(6):
+                    er = np.full((S, m), -1, dtype=np.int32)
+                    for s in range(S):
+                        tt = int(rng.integers(1, m + 1))
+                        er[s, :tt] = rng.choice(k + m, tt, replace=False)
+                    d = torch.from_numpy(refs[t]).cuda()
+                    for s in range(S):
+                        for b in er[s]:
+                            if b >= 0:
+                                d[s, int(b)] = 0
+                    plan.decode_batch(d, er, stream=stream)
+                    d2 = torch.from_numpy(refs[t]).cuda()
+                    d2[:, k:] = 0
+                    plan.encode_batch(d2, stream=stream)
+                    stream.synchronize()
+                    if not (np.array_equal(d.cpu().numpy(), refs[t]) and np.array_equal(d2.cpu().numpy(), refs[t])):
+                        errs.append((t, it))
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
