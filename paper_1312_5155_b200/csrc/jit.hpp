@@ -55,9 +55,10 @@ struct Args {
   const uint64_t *ptrs;
   int n;
   int pad;
-  const int32_t *stripes;  // selected stripe indices (nullptr = 0..n_sel-1)
+  const int32_t *stripes;  // selected stripe indices (nullptr = stripe_base .. stripe_base+n_sel-1)
   uint64_t n_sel, units_per_stripe;
   uint32_t units_per_cta, ctas_per_stripe;
+  uint64_t stripe_base;
 };
 
 bool available(std::string *why = nullptr);

@@ -170,7 +170,15 @@ struct rs_poly_plan {
     size_t cap = 0;
   };
   mutable std::map<int, std::unique_ptr<Staging>> staging;
+  mutable std::map<int, uint8_t *> enc_dev;  // device -> encode tail constants
   ~rs_poly_plan() {
+    for (auto &kv : enc_dev) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(kv.first);
+      cudaFree(kv.second);
+      cudaSetDevice(cur);
+    }
     for (auto &kv : staging)
       if (kv.second->p) {
         int cur = 0;
@@ -507,8 +515,9 @@ uint32_t units_per_cta_for(uint64_t total) {
 }
 
 cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32_t *stripes, uint64_t n_sel,
-                       uint64_t body_units, cudaStream_t st, bool pdl = false) {
+                       uint64_t body_units, cudaStream_t st, bool pdl = false, uint64_t stripe_base = 0) {
   rsb::jit::Args a{};
+  a.stripe_base = stripe_base;
   a.base = G.L.base;
   a.stripe_stride = G.L.stripe_stride;
   a.block_stride = G.L.block_stride;
@@ -655,6 +664,30 @@ rs_status check_geometry(const rs_poly_plan *P, size_t block_bytes) {
   return RS_OK;
 }
 
+// Device copy of the encode tail constants [GenericPat | tables], made once per plan and
+// device (synchronous upload: later calls on any stream see it).
+constexpr size_t kEncTablesOff = (sizeof(rsb::GenericPat) + 15) & ~(size_t)15;
+const uint8_t *enc_consts(const rs_poly_plan &P) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(P.mu);
+  auto it = P.enc_dev.find(dev);
+  if (it != P.enc_dev.end()) return it->second;
+  std::vector<uint8_t> h(kEncTablesOff + P.enc_tab.size(), 0);
+  rsb::GenericPat gp = P.enc_gp;
+  gp.table_off = 0;
+  std::memcpy(h.data(), &gp, sizeof(gp));
+  std::memcpy(h.data() + kEncTablesOff, P.enc_tab.data(), P.enc_tab.size());
+  uint8_t *d = nullptr;
+  if (cudaMalloc(reinterpret_cast<void **>(&d), h.size()) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  P.enc_dev.emplace(dev, d);
+  return d;
+}
+
 rs_status encode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs, cudaStream_t st) {
   const rsb::jit::Kernel *jk = nullptr;
   uint64_t body = body_units_of(*P, G);
@@ -665,27 +698,31 @@ rs_status encode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs, c
     jk = jit_get(*P, kEncodeKey, [&] { return encoder_spec(*P); }, false);
   }
   if (!P->sliced && !jk) body = 0;
-  Blob b;
-  size_t ptrs_off = SIZE_MAX;
-  if (ptrs) ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
-  rsb::GenericPat gp = P->enc_gp;
-  gp.table_off = 0;
-  const size_t pats_off = b.add(&gp, sizeof(gp));
-  const size_t tables_off = b.add(P->enc_tab.data(), P->enc_tab.size());
+  // Per call only the pointer table (pointer mode) is uploaded; the encode constants of the
+  // generic tail kernel are plan-static and live on the device once per plan and device.
+  const uint64_t UB0 = 32ull * (uint64_t)P->w / 8;
+  const bool tail = body * UB0 < G.block_bytes;
+  const uint8_t *cdev = nullptr;
+  if (tail && !(cdev = enc_consts(*P))) return RS_ERR_CUDA;
+  const size_t pats_off = 0, tables_off = kEncTablesOff;
   DevBlob d;
-  cudaError_t e = d.upload(*P, b, st);
-  if (e == cudaSuccess && ptrs) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
+  cudaError_t e = cudaSuccess;
+  if (ptrs) {
+    Blob b;
+    b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
+    e = d.upload(*P, b, st);
+    if (e == cudaSuccess) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p);
+  }
   if (e == cudaSuccess && body) {
     if (P->sliced) {
-      e = launch_sliced_body(*P, false, G, body, d.p, 0, 0, 0, st);
+      e = launch_sliced_body(*P, false, G, body, nullptr, 0, 0, 0, st);
     } else {
       e = launch_jit(*jk, G, nullptr, G.n_stripes, body, st);
       P->jit_launches++;
     }
   }
-  const uint64_t UB = 32ull * (uint64_t)P->w / 8;
-  if (e == cudaSuccess)
-    e = launch_generic_range(*P, G, body * UB, G.block_bytes, d.p, pats_off, SIZE_MAX, tables_off,
+  if (e == cudaSuccess && tail)
+    e = launch_generic_range(*P, G, body * UB0, G.block_bytes, cdev, pats_off, SIZE_MAX, tables_off,
                              (uint32_t)((P->m + 3) / 4), (uint32_t)(P->k * (P->w == 8 ? 128 : 512)), st);
   cudaError_t ef = d.release();
   return cuda_status(e != cudaSuccess ? e : ef);
@@ -902,6 +939,23 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
     } else {
       any_rt = true;
     }
+  }
+  // Lean path: every pattern has its JIT kernel, no ragged tail, strided layout and each
+  // pattern's stripes contiguous (one stripe, or one shared pattern) -- nothing to upload,
+  // the kernels take the stripe range by value.
+  bool contig = true;
+  for (const auto &gr : groups)
+    for (size_t q = 1; q < gr.size() && contig; ++q) contig = gr[q] == gr[0] + (int32_t)q;
+  if (any_jit && !any_rt && !ptrs && contig && body * UB == G.block_bytes && side_streams(*P).empty()) {
+    cudaError_t e = cudaSuccess;
+    bool first = true;
+    for (size_t i = 0; i < pats.size() && e == cudaSuccess; ++i) {
+      if (groups[i].empty()) continue;
+      e = launch_jit(*jk[i], G, nullptr, groups[i].size(), body, st, !first, (uint64_t)groups[i][0]);
+      first = false;
+      P->jit_launches++;
+    }
+    return cuda_status(e);
   }
   Blob b;
   size_t ptrs_off = SIZE_MAX;
