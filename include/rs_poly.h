@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define RS_POLY_ABI_VERSION 1
+#define RS_POLY_ABI_VERSION 2 /* 2: rs_poly_stats.jit_cache_hits */
 #define RS_POLY_MAX_N 255 /* k+m <= 255 (also k+m <= 2^w-1, reading G7) */
 #define RS_POLY_MAX_M 32
 
@@ -235,6 +235,9 @@ typedef struct {
   uint64_t table_launches; /* decode body launches that used the table kernels    */
   int jit_available;       /* 1 if NVRTC could be loaded                          */
   int jit_mode;
+  uint64_t jit_cache_hits; /* ready JIT kernels loaded from the on-disk cubin cache
+                              ($RS_POLY_JIT_CACHE, else ~/.cache/rs_poly_jit; "off"
+                              disables it) instead of being compiled               */
 } rs_poly_stats;
 rs_status rs_poly_plan_stats(const rs_poly_plan *plan, rs_poly_stats *out);
 

@@ -44,6 +44,7 @@ struct Kernel {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t fn = nullptr;
   int xors = 0;
+  bool cached = false;  // loaded from the on-disk cubin cache
   double compile_ms = 0;
   std::string log;
 };

@@ -1382,8 +1382,12 @@ rs_status rs_poly_plan_stats(const rs_poly_plan *P, rs_poly_stats *out) {
   out->patterns = P->cache.size();
   for (auto &kv : P->jit) {
     if (!kv.second->ready()) out->jit_pending++;
-    else if (kv.second->kernel()) out->jit_ready++;
-    else out->jit_failed++;
+    else if (const rsb::jit::Kernel *kk = kv.second->kernel()) {
+      out->jit_ready++;
+      out->jit_cache_hits += kk->cached ? 1 : 0;
+    } else {
+      out->jit_failed++;
+    }
   }
   out->jit_launches = P->jit_launches.load();
   out->table_launches = P->table_launches.load();

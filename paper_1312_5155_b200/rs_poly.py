@@ -55,7 +55,8 @@ _lib.rs_poly_xor_reduce.argtypes = [_vp, _vp, _vp, _i32, _sz, _sz, _vp]
 class Stats(ctypes.Structure):
     """rs_poly_stats"""
     _fields_ = [("patterns", _u64), ("jit_ready", _u64), ("jit_pending", _u64), ("jit_failed", _u64),
-                ("jit_launches", _u64), ("table_launches", _u64), ("jit_available", _i32), ("jit_mode", _i32)]
+                ("jit_launches", _u64), ("table_launches", _u64), ("jit_available", _i32), ("jit_mode", _i32),
+                ("jit_cache_hits", _u64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

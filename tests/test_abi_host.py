@@ -48,7 +48,7 @@ def test_every_declared_symbol_is_exported(rs):
 
 
 def test_abi_version_and_strerror(rs):
-    assert rs.abi_version() == 1
+    assert rs.abi_version() == 2
     for s in range(8):
         assert rs.strerror(s)
     assert "unknown" in rs.strerror(99)

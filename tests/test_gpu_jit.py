@@ -187,3 +187,31 @@ def test_concurrent_host_threads_share_a_plan():
     for t in ts:
         t.join()
     assert not errs, errs
+
+
+def test_jit_disk_cache(tmp_path, monkeypatch):
+    """Second plan, same patterns: kernels come from the on-disk cubin cache, same bytes."""
+    import time
+    monkeypatch.setenv("RS_POLY_JIT_CACHE", str(tmp_path))
+    k, m, B, S = 12, 4, 16384, 6
+    ref = encoded(k, m, 16, P16, B, S, seed=60)
+    er = synth.erasure_table("C4", 9, S)
+    m_ = rs()
+    p1 = m_.Plan(k, m, 16, P16)
+    t0 = time.perf_counter()
+    p1.prepare(er)
+    t_compile = time.perf_counter() - t0
+    assert p1.stats()["jit_cache_hits"] == 0 and len(list(tmp_path.iterdir())) >= 1
+    p2 = m_.Plan(k, m, 16, P16)
+    t0 = time.perf_counter()
+    p2.prepare(er)
+    t_cached = time.perf_counter() - t0
+    st = p2.stats()
+    assert st["jit_cache_hits"] == st["jit_ready"] > 0
+    assert t_cached < t_compile
+    d = torch.from_numpy(ref).cuda()
+    for s in range(S):
+        d[s, torch.from_numpy(er[s].astype(np.int64)).cuda()] = 0
+    p2.decode_batch(d, er)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
