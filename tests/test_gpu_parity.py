@@ -257,3 +257,54 @@ def test_launch_counter_moves():
     plan.encode_batch(d)
     torch.cuda.synchronize()
     assert m.launch_count() > before
+
+
+@pytest.mark.parametrize("k,m,w,poly,B", [(223, 32, 8, P8, 777), (240, 15, 8, P8, 64), (1, 1, 8, P8, 1),
+                                          (3, 2, 16, P16, 2), (100, 32, 16, P16, 34)])
+def test_extreme_geometries(k, m, w, poly, B):
+    """Maximum n = 255 (w8) and m = 32, one-symbol blocks: encode and an m-erasure decode."""
+    S = 2
+    ref = oracle_encoded(host_stripes(k, m, B, S, seed=8), k, m, w, poly)
+    plan = rs().Plan(k, m, w, poly)
+    d = to_dev(ref)
+    d[:, k:] = 0
+    plan.encode_batch(d)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    rng = np.random.default_rng(k)
+    er = np.stack([np.sort(rng.choice(k + m, m, replace=False)) for _ in range(S)]).astype(np.int32)
+    for s in range(S):
+        d[s, torch.from_numpy(er[s].astype(np.int64)).cuda()] = 0x99
+    plan.decode_batch(d, er)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("k,m,w,poly,B", [(10, 4, 8, P8, 4096 + 40), (12, 4, 16, P16, 8192 + 6), (5, 2, 8, P8, 999)])
+def test_no_writes_outside_blocks(k, m, w, poly, B):
+    """Every block sits between canary bytes (padding of the block and stripe strides); encode,
+    decode (JIT and table paths), diff-update and the XOR reduction leave the canaries intact."""
+    import paper_1312_5155_b200 as mod
+    S, pad = 3, 96
+    ref = oracle_encoded(host_stripes(k, m, B, S, seed=9), k, m, w, poly)
+    for jit in (mod.RS_JIT_SYNC, mod.RS_JIT_OFF):
+        big = torch.full((S, k + m, B + pad), 0xA7, dtype=torch.uint8, device="cuda")
+        view = big[:, :, :B]
+        view.copy_(torch.from_numpy(ref))
+        view[:, k:] = 0
+        plan = mod.Plan(k, m, w, poly)
+        plan.set_jit(jit)
+        plan.encode_batch(view)
+        er = np.array([[0, k, -1, -1][:m] + [-1] * (m - 2)] * S, dtype=np.int32)[:, :m]
+        for s in range(S):
+            view[s, torch.from_numpy(er[s][er[s] >= 0].astype(np.int64)).cuda()] = 0
+        plan.decode_batch(view, er)
+        old = view[:, [1]].clone()
+        view[:, 1] ^= 0x5C
+        plan.update_batch(view, [1], old)
+        view[:, 1] ^= 0x5C
+        plan.update_batch(view, [1], old ^ 0x5C)
+        plan.xor_reduce([view[s, 0] for s in range(S)], [[view[s, 0], view[s, 2], view[s, 2]] for s in range(S)], B)
+        torch.cuda.synchronize()
+        assert np.array_equal(view.cpu().numpy(), ref)
+        assert bool((big[:, :, B:] == 0xA7).all()), "write outside a block"
