@@ -474,17 +474,21 @@ std::vector<cudaStream_t> side_streams(const rs_poly_plan &P) {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(P.mu);
   auto &v = P.pool[dev];
-  static const size_t want = [] {
-    const char *e = std::getenv("RS_POLY_SIDE_STREAMS");  // tuning knob; default 0 (PDL chain)
-    const long v = e ? std::strtol(e, nullptr, 10) : 0;
-    return (size_t)std::max(0L, std::min(v, 63L));
+  // Extra PDL chains for the per-pattern JIT launches.  Default: one extra for w = 8 (two
+  // ~20 KB kernels share an SM well: C3 decode 89% -> 96%), none for w = 16 (two ~60 KB
+  // kernels thrash the instruction cache: C4 78% -> 56%).  RS_POLY_SIDE_STREAMS overrides.
+  static const long env = [] {
+    const char *e = std::getenv("RS_POLY_SIDE_STREAMS");
+    return e ? std::max(0L, std::min(std::strtol(e, nullptr, 10), 63L)) : -1L;
   }();
+  const size_t want = env >= 0 ? (size_t)env : (P.w == 8 ? 1 : 0);
+  if (want == 0) return {};
   while (v.size() < want) {
     cudaStream_t s = nullptr;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) break;
     v.push_back(s);
   }
-  return v;
+  return std::vector<cudaStream_t>(v.begin(), v.begin() + std::min(want, v.size()));
 }
 
 uint64_t body_units_of(const rs_poly_plan &P, const Geometry &G) {
@@ -508,7 +512,12 @@ int sm_count() {
 // Units (32 columns each) per CTA for a launch over `total` units: up to kSlicedUnitsPerCta,
 // fewer when that would leave less than ~8 CTAs per SM (single stripes, per-pattern launches).
 uint32_t units_per_cta_for(uint64_t total) {
-  const uint64_t target = (uint64_t)sm_count() * 8;
+  static const uint64_t per_sm = [] {  // tuning knob RS_POLY_CTAS_PER_SM (default 8)
+    const char *e = std::getenv("RS_POLY_CTAS_PER_SM");
+    const long v = e ? std::strtol(e, nullptr, 10) : 8;
+    return (uint64_t)std::max(1L, std::min(v, 64L));
+  }();
+  const uint64_t target = (uint64_t)sm_count() * per_sm;
   uint64_t upc = (total + target - 1) / target;
   upc = (upc + kSlicedThreads - 1) / kSlicedThreads * kSlicedThreads;
   return (uint32_t)std::min<uint64_t>(std::max<uint64_t>(upc, kSlicedThreads), kSlicedUnitsPerCta);
@@ -906,6 +915,59 @@ const rsb::jit::Kernel *pattern_jit(const rs_poly_plan &P, const PatternHost &ph
   return jit_get(P, JitKey{kJitDecode, key}, [&] { return decoder_spec(P, ph); }, wait);
 }
 
+// The per-pattern JIT kernels of one decode call, one launch per pattern (its stripes).
+// Launches form programmatic-dependent-launch chains: each generated kernel triggers its
+// dependents on entry and waits for its predecessor before exit, so kernel i+1's CTAs
+// fill kernel i's last wave (a C4 stripe is only ~2.3 waves) while completion stays in
+// stream order.  The first kernel of a chain is launched without the attribute, so it
+// never overlaps work queued before the call.  With side streams (side_streams()), the
+// patterns are dealt round-robin over 1 + N chains forked from and joined back to `st`.
+// dev_lists: device base of the per-pattern stripe lists (grp_off), or nullptr when every
+// group is a contiguous stripe range (passed by value).
+cudaError_t launch_jit_chains(const rs_poly_plan &P, const std::vector<const rsb::jit::Kernel *> &jk,
+                              const std::vector<std::vector<int32_t>> &groups, const Geometry &G, uint64_t body,
+                              const uint8_t *dev_lists, const std::vector<size_t> &grp_off, cudaStream_t st) {
+  size_t nlaunch = 0;
+  for (const auto &g : groups) nlaunch += g.empty() ? 0 : 1;
+  std::vector<cudaStream_t> side = nlaunch > 1 ? side_streams(P) : std::vector<cudaStream_t>{};
+  cudaError_t e = cudaSuccess;
+  cudaEvent_t fork = nullptr;
+  if (!side.empty()) {
+    e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(fork, st);
+  }
+  std::vector<char> used(side.size(), 0), chained(side.size() + 1, 0);
+  size_t rr = 0;
+  for (size_t i = 0; i < groups.size() && e == cudaSuccess; ++i) {
+    if (groups[i].empty()) continue;
+    const size_t lane = rr++ % (side.size() + 1);
+    cudaStream_t s = lane == 0 ? st : side[lane - 1];
+    if (lane && !used[lane - 1]) {
+      e = cudaStreamWaitEvent(s, fork, 0);
+      used[lane - 1] = 1;
+    }
+    if (e != cudaSuccess) break;
+    if (dev_lists)
+      e = launch_jit(*jk[i], G, reinterpret_cast<const int32_t *>(dev_lists + grp_off[i]), groups[i].size(), body,
+                     s, chained[lane] != 0);
+    else
+      e = launch_jit(*jk[i], G, nullptr, groups[i].size(), body, s, chained[lane] != 0, (uint64_t)groups[i][0]);
+    chained[lane] = 1;
+    P.jit_launches++;
+  }
+  for (size_t l = 0; l < side.size(); ++l) {
+    if (!used[l]) continue;
+    cudaEvent_t join = nullptr;
+    cudaError_t e2 = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    if (e2 == cudaSuccess) e2 = cudaEventRecord(join, side[l]);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, join, 0);
+    if (join) cudaEventDestroy(join);
+    if (e == cudaSuccess) e = e2;
+  }
+  if (fork) cudaEventDestroy(fork);
+  return e;
+}
+
 // rows: per stripe list of erased API indices (validated, sorted ascending)
 rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
                       const std::vector<std::vector<int>> &rows, cudaStream_t st) {
@@ -946,17 +1008,8 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   bool contig = true;
   for (const auto &gr : groups)
     for (size_t q = 1; q < gr.size() && contig; ++q) contig = gr[q] == gr[0] + (int32_t)q;
-  if (any_jit && !any_rt && !ptrs && contig && body * UB == G.block_bytes && side_streams(*P).empty()) {
-    cudaError_t e = cudaSuccess;
-    bool first = true;
-    for (size_t i = 0; i < pats.size() && e == cudaSuccess; ++i) {
-      if (groups[i].empty()) continue;
-      e = launch_jit(*jk[i], G, nullptr, groups[i].size(), body, st, !first, (uint64_t)groups[i][0]);
-      first = false;
-      P->jit_launches++;
-    }
-    return cuda_status(e);
-  }
+  if (any_jit && !any_rt && !ptrs && contig && body * UB == G.block_bytes)
+    return cuda_status(launch_jit_chains(*P, jk, groups, G, body, nullptr, {}, st));
   Blob b;
   size_t ptrs_off = SIZE_MAX;
   if (ptrs) ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
@@ -1000,50 +1053,7 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   if (e == cudaSuccess)
     e = launch_generic_range(*P, G, body * UB, G.block_bytes, d.p, generic_pats_off, idx_off, tables_off,
                              max_groups, smem, st);
-  // JIT kernels, one launch per pattern.  Default: one chain on the caller's stream with
-  // programmatic dependent launch, so each kernel's last wave overlaps the next kernel's
-  // first (a C4 stripe is only ~2.3 waves).  The first kernel of the chain is launched
-  // without the attribute: it must not overlap the work queued before this call.
-  // RS_POLY_SIDE_STREAMS=N > 0 instead spreads the launches over N extra streams.
-  if (e == cudaSuccess && any_jit && side_streams(*P).empty()) {
-    bool first = true;
-    for (size_t i = 0; i < pats.size() && e == cudaSuccess; ++i) {
-      if (groups[i].empty()) continue;
-      e = launch_jit(*jk[i], G, reinterpret_cast<const int32_t *>(d.p + grp_off[i]), groups[i].size(), body, st,
-                     !first);
-      first = false;
-      P->jit_launches++;
-    }
-  } else if (e == cudaSuccess && any_jit) {
-    std::vector<cudaStream_t> side = side_streams(*P);
-    cudaEvent_t fork = nullptr;
-    e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventRecord(fork, st);
-    std::vector<char> used(side.size(), 0);
-    size_t rr = 0;
-    for (size_t i = 0; i < pats.size() && e == cudaSuccess; ++i) {
-      if (groups[i].empty()) continue;
-      const size_t lane = rr++ % (side.size() + 1);
-      cudaStream_t s = lane == 0 ? st : side[lane - 1];
-      if (lane && !used[lane - 1]) {
-        e = cudaStreamWaitEvent(s, fork, 0);
-        used[lane - 1] = 1;
-      }
-      if (e == cudaSuccess)
-        e = launch_jit(*jk[i], G, reinterpret_cast<const int32_t *>(d.p + grp_off[i]), groups[i].size(), body, s);
-      P->jit_launches++;
-    }
-    for (size_t l = 0; l < side.size(); ++l) {
-      if (!used[l]) continue;
-      cudaEvent_t join = nullptr;
-      cudaError_t e2 = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
-      if (e2 == cudaSuccess) e2 = cudaEventRecord(join, side[l]);
-      if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, join, 0);
-      if (join) cudaEventDestroy(join);
-      if (e == cudaSuccess) e = e2;
-    }
-    if (fork) cudaEventDestroy(fork);
-  }
+  if (e == cudaSuccess && any_jit) e = launch_jit_chains(*P, jk, groups, G, body, d.p, grp_off, st);
   cudaError_t ef = d.release();
   return cuda_status(e != cudaSuccess ? e : ef);
 }
