@@ -33,10 +33,6 @@ struct Spec {
   uint32_t poly = 0;
   std::vector<int> seq;
   int T = 0;
-  // loop_positions: emit the positions after the first survivor as a runtime loop
-  // (seq[i] is at position pos_top - i; block of a position: data pos-m, parity k+pos)
-  bool loop_positions = false;
-  int pos_top = 0, k = 0, m = 0;
 };
 
 struct Kernel {

@@ -370,14 +370,6 @@ rsb::jit::Spec jit_spec(const rs_poly_plan &P, const std::vector<int> &in, const
   return s;
 }
 
-// Syndrome-form JIT kernels are fully unrolled (compile-time erased set; loads of all
-// positions in flight).  RS_POLY_JIT_LOOP=1 emits a compact position loop instead
-// (measured slower on C4: 9.2 vs 6.6 ms -- one block in flight per thread).
-bool jit_loop_positions() {
-  static const bool v = std::getenv("RS_POLY_JIT_LOOP") && std::getenv("RS_POLY_JIT_LOOP")[0] == '1';
-  return v;
-}
-
 // The encoder kernel of a code without a compiled network: w = 8 the parity-map
 // network, w = 16 the syndrome form (Horner over the data, then Q).
 rsb::jit::Spec encoder_spec(const rs_poly_plan &P) {
@@ -392,10 +384,6 @@ rsb::jit::Spec encoder_spec(const rs_poly_plan &P) {
     s.M = rsb::horner_q(P.F, P.m);
     for (int j = P.k - 1; j >= 0; --j) s.seq.push_back(j);  // positions m+k-1 .. m
     s.min_blocks = 3;
-    s.loop_positions = jit_loop_positions();
-    s.pos_top = P.m + P.k - 1;
-    s.k = P.k;
-    s.m = P.m;
   }
   return s;
 }
@@ -416,10 +404,6 @@ rsb::jit::Spec decoder_spec(const rs_poly_plan &P, const PatternHost &ph) {
       s.seq.push_back(er[b] ? -1 : b);
     }
     s.min_blocks = 3;
-    s.loop_positions = jit_loop_positions();
-    s.pos_top = P.n - 1;
-    s.k = P.k;
-    s.m = P.m;
   }
   return s;
 }
