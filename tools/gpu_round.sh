@@ -13,3 +13,5 @@ for cfg in C5 C4; do
   python tools/profile_kernel.py --config $cfg --stripes 32 > gpurun_out/${tag}_plain_$cfg.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"sliced_kernel|rs_jit" -s 33 -c 3 -o gpurun_out/${tag}_prof_$cfg python tools/profile_kernel.py --config $cfg --stripes 32 > gpurun_out/${tag}_ncu_$cfg.log 2>&1; echo "ncu $cfg rc=$?"
 done
+python tools/bench_next.py update --steps 2 --warmup 1 > gpurun_out/${tag}_plain_upd.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:rs_jit -s 1 -c 1 -o gpurun_out/${tag}_prof_update python tools/bench_next.py update --steps 2 --warmup 1 > gpurun_out/${tag}_ncu_upd.log 2>&1; echo "ncu update rc=$?"
