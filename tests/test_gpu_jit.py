@@ -215,3 +215,35 @@ def test_jit_disk_cache(tmp_path, monkeypatch):
     p2.decode_batch(d, er)
     torch.cuda.synchronize()
     assert np.array_equal(d.cpu().numpy(), ref)
+
+
+def test_stress_many_patterns_repeated():
+    """30 decode calls over 256 stripes with fresh random per-stripe patterns each time (PDL
+    chains over two streams, table fallback while kernels compile), interleaved with encodes
+    and diff-updates on the same stream: every byte right every time."""
+    k, m, B, S = 10, 4, 16 * 1024 + 32, 256
+    m_ = rs()
+    plan = m_.Plan(k, m)
+    ref = encoded(k, m, 8, P8, B, S, seed=70)
+    d = torch.from_numpy(ref).cuda()
+    golden = d.clone()
+    rng = np.random.default_rng(70)
+    for it in range(30):
+        er = np.full((S, m), -1, dtype=np.int32)
+        for s in range(S):
+            t = int(rng.integers(1, m + 1))
+            er[s, :t] = np.sort(rng.choice(k + m, t, replace=False))
+        mask = torch.zeros((S, k + m), dtype=torch.bool, device="cuda")
+        for s in range(S):
+            mask[s, torch.from_numpy(er[s][er[s] >= 0].astype(np.int64)).cuda()] = True
+        d[mask] = 0x11
+        plan.decode_batch(d, er)
+        if it % 3 == 0:
+            plan.encode_batch(d)
+        if it % 5 == 0:
+            old = d[:, [2]].clone()
+            d[:, 2] ^= 0x3C
+            plan.update_batch(d, [2], old)
+            d[:, 2] ^= 0x3C
+            plan.update_batch(d, [2], old ^ 0x3C)
+        assert torch.equal(d, golden), f"iteration {it}"
