@@ -27,6 +27,11 @@
 
 namespace rsb {
 
+#ifndef RS_W16_HUNROLL
+#define RS_W16_HUNROLL 3  // Horner over the data blocks unrolled by 3 (0: fully; C4 encode 86% -> 88.5%:
+                          // a 40 KB fully unrolled loop body stalls on instruction fetch)
+#endif
+
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launches_total() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1); }
@@ -67,12 +72,30 @@ __device__ __forceinline__ void horner_all(uint32_t (&h)[M * W], const uint32_t 
   if constexpr (J + 1 < M) horner_all<K, M, W, POLY, DECODE, J + 1>(h, c);
 }
 
+constexpr int kHornerUnroll = RS_W16_HUNROLL > 0 ? RS_W16_HUNROLL : 1;
+
 template <int K, int M, int W, uint32_t POLY, bool DECODE>
 __device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off, uint32_t emask,
                                               uint32_t (&y)[M * W]) {
   uint32_t h[M * W];
+  {
+    uint32_t c[W];
+    if (DECODE && ((emask >> (K - 1)) & 1u)) {
 #pragma unroll
-  for (int jb = K - 1; jb >= 0; --jb) {
+      for (int q = 0; q < W; ++q) c[q] = 0;
+    } else {
+      load_unit<W>(blk[K - 1] + off, c);
+      transposeW<W>(c);
+    }
+#pragma unroll
+    for (int i = 0; i < M * W; ++i) h[i] = c[i % W];
+  }
+#if RS_W16_HUNROLL
+#pragma unroll kHornerUnroll
+#else
+#pragma unroll
+#endif
+  for (int jb = K - 2; jb >= 0; --jb) {
     uint32_t c[W];
     if (DECODE && ((emask >> jb) & 1u)) {
 #pragma unroll
@@ -81,12 +104,7 @@ __device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off,
       load_unit<W>(blk[jb] + off, c);
       transposeW<W>(c);
     }
-    if (jb == K - 1) {
-#pragma unroll
-      for (int i = 0; i < M * W; ++i) h[i] = c[i % W];
-    } else {
-      horner_all<K, M, W, POLY, DECODE, 0>(h, c);
-    }
+    horner_all<K, M, W, POLY, DECODE, 0>(h, c);
   }
   RsQNet<K, M, W, POLY>::run(h, y);
 }
