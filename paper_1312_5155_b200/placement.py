@@ -17,6 +17,11 @@ The result equals rs_poly_encode of the whole stripe (tests/test_dist_placement.
 against the oracle with gloo ranks; tests/test_gpu_placement.py runs the GPU kernels with
 in-process ranks).  The byte traffic and the alternatives are discussed in DESIGN.md §8.
 
+``encode_distributed_p2p`` is the fused variant: every rank's receive buffer is mapped into
+its peers (torch symmetric memory over NVLink / NVSwitch), and the partial-encode kernel's
+output pointers for a remote owner are the owner's receive slots -- the kernel's stores are
+the transfer, overlapping the math tile by tile; one barrier, then the owners' XOR.
+
 ``ops`` supplies the compute steps; the default is the CUDA library (``Plan``).  Tests of the
 host-side protocol inject CPU implementations -- the product path itself has no CPU fallback.
 """
@@ -122,3 +127,75 @@ def encode_distributed(lay: Layout, store: dict, S: int, nbytes: int, rank: int,
         ops.xor_reduce(dst, srcs, nbytes)
     return {"sent_blocks": sum(in_splits), "received_blocks": sum(out_splits),
             "local_partial_calls": len(groups), "xor_calls": len(by_n)}
+
+
+def recv_slots(lay: Layout, dst: int, S: int) -> dict:
+    """Row of every partial (src, stripe, parity index) in rank `dst`'s receive buffer
+    (sources in rank order, then the wire order of Layout.sends)."""
+    rows = {}
+    for src in range(lay.world):
+        for s, i in lay.sends(src, dst, S):
+            rows[(src, s, i)] = len(rows)
+    return rows
+
+
+def encode_distributed_p2p(lay: Layout, store: dict, S: int, nbytes: int, rank: int, peer_recv: list,
+                           barrier, ops) -> dict:
+    """SPMD, fused compute + transfer.  `peer_recv[r]` is rank r's receive buffer ([rows,
+    nbytes]; rows >= len(recv_slots(lay, r, S))) as seen from this rank -- a peer-mapped
+    view (symmetric memory) on GPUs.  `barrier()` returns once every rank's partial stores
+    are complete and visible.  Same result as encode_distributed."""
+    k, m, N = lay.k, lay.m, lay.world
+    like = next(iter(store.values()))
+    slots = [recv_slots(lay, d, S) for d in range(N)]
+    junk = ops.empty(1, nbytes, like)[0]
+    groups: dict[tuple, list[int]] = {}
+    for s in range(S):
+        groups.setdefault(tuple(lay.data_on(rank, s)), []).append(s)
+    sent = 0
+    for idx, stripes in groups.items():
+        data = [[store[(s, j)] for j in idx] for s in stripes]
+        partial = []
+        for s in stripes:
+            row = []
+            for i in range(m):
+                d = lay.parity_owner(i, s)
+                if d == rank:
+                    row.append(store[(s, k + i)])
+                elif idx:
+                    row.append(peer_recv[d][slots[d][(rank, s, i)]])   # the store goes over NVLink
+                    sent += 1
+                else:
+                    row.append(junk)
+            partial.append(row)
+        ops.encode_partial(list(idx), data, partial, nbytes)
+    barrier()
+    mine = peer_recv[rank]
+    got: dict[tuple[int, int], list] = {}
+    for (src, s, i), r in slots[rank].items():
+        got.setdefault((s, i), []).append(mine[r])
+    by_n: dict[int, list] = {}
+    for (s, i), parts in got.items():
+        by_n.setdefault(len(parts), []).append((s, i, parts))
+    for nsrc, items in by_n.items():
+        ops.xor_reduce([store[(s, k + i)] for s, i, _ in items],
+                       [[store[(s, k + i)]] + parts for s, i, parts in items], nbytes)
+    return {"sent_blocks": sent, "received_blocks": len(slots[rank]), "local_partial_calls": len(groups),
+            "xor_calls": len(by_n)}
+
+
+def symmetric_recv_buffers(lay: Layout, S: int, nbytes: int, group=None):
+    """Allocate this rank's receive buffer in symmetric memory and return (views of every
+    rank's buffer as mapped here, device barrier).  Needs CUDA peer access (NVLink)."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    rows = max(max(len(recv_slots(lay, d, S)) for d in range(lay.world)), 1)
+    buf = symm_mem.empty((rows, nbytes), dtype=torch.uint8, device=torch.cuda.current_device())
+    hdl = symm_mem.rendezvous(buf, group or dist.group.WORLD)
+    views = [buf if r == hdl.rank else hdl.get_buffer(r, (rows, nbytes), torch.uint8) for r in range(lay.world)]
+
+    def barrier():
+        hdl.barrier(channel=0)   # every rank's stores issued before it on its stream are visible
+
+    return views, barrier

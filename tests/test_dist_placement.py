@@ -96,3 +96,43 @@ def test_layout_owner_rotation():
         assert sorted(b for r in range(8) for b in lay.blocks_on(r, s)) == list(range(14))
     owners = [lay.parity_owner(i, s) for s in range(8) for i in range(4)]
     assert sorted(set(owners)) == list(range(8))          # rotation spreads parity ownership
+
+
+def _worker_p2p(rank, world, k, m, S, B, port, recv_bufs, q):
+    """Fused variant: partials are stored straight into the owners' receive buffers (here
+    shared-memory tensors standing in for NVLink-mapped peer memory)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1312_5155_b200.placement import Layout, encode_distributed_p2p
+    lay = Layout(k, m, world)
+    full = synth.stripes_array(4, range(S), k, m, B)
+    store = {}
+    for s in range(S):
+        for b in lay.blocks_on(rank, s):
+            store[(s, b)] = torch.from_numpy(full[s, b].copy()) if b < k else torch.full((B,), 0xCD, dtype=torch.uint8)
+    stats = encode_distributed_p2p(lay, store, S, B, rank, recv_bufs, dist.barrier, OracleOps(k, m))
+    ref = full.copy()
+    oracle.encode_bulk(ref, k, m, 8, P8)
+    bad = sum(int(not np.array_equal(t.numpy(), ref[s, b])) for (s, b), t in store.items())
+    q.put((rank, bad, stats))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,m", [(2, 10, 4), (3, 6, 3), (4, 2, 2)])
+def test_placement_p2p_protocol_gloo(world, k, m):
+    from paper_1312_5155_b200.placement import Layout, recv_slots
+    S, B = 7, 64
+    lay = Layout(k, m, world)
+    rows = max(1, max(len(recv_slots(lay, d, S)) for d in range(world)))
+    bufs = [torch.zeros((rows, B), dtype=torch.uint8).share_memory_() for _ in range(world)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + world * 7 + k
+    ps = [ctx.Process(target=_worker_p2p, args=(r, world, k, m, S, B, port, bufs, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(bad == 0 for _, bad, _ in res), res
+    assert sum(st["sent_blocks"] for _, _, st in res) == sum(st["received_blocks"] for _, _, st in res)

@@ -103,3 +103,46 @@ def test_placement_protocol_on_gpu(world, k, m):
     for r in range(world):
         for (s, b), t in stores[r].items():
             assert np.array_equal(t.cpu().numpy(), ref[s, b]), (r, s, b)
+
+
+@pytest.mark.parametrize("world,k,m", [(4, 10, 4), (8, 6, 3)])
+def test_placement_p2p_on_gpu(world, k, m):
+    """Fused variant with the CUDA kernels: the partial-encode kernel writes straight into the
+    owners' receive buffers (device tensors standing in for peer-mapped memory)."""
+    from paper_1312_5155_b200.placement import CudaOps, Layout, encode_distributed_p2p, recv_slots
+    S, B = 9, 32 * 1024
+    lay = Layout(k, m, world)
+    full = synth.stripes_array(7, range(S), k, m, B)
+    ref = full.copy()
+    oracle.encode_bulk(ref, k, m, 8, P8, threads=4)
+    m_ = rs()
+    rows = max(1, max(len(recv_slots(lay, d, S)) for d in range(world)))
+    bufs = [torch.zeros((rows, B), dtype=torch.uint8, device="cuda") for _ in range(world)]
+    stores = [{(s, b): (torch.from_numpy(full[s, b].copy()).cuda() if b < k else
+                        torch.full((B,), 0xCD, dtype=torch.uint8, device="cuda"))
+               for s in range(S) for b in lay.blocks_on(r, s)} for r in range(world)]
+    bar = threading.Barrier(world)
+
+    def barrier():
+        torch.cuda.synchronize()
+        bar.wait()
+
+    errs = []
+
+    def run(r):
+        try:
+            encode_distributed_p2p(lay, stores[r], S, B, r, bufs, barrier, CudaOps(m_.Plan(k, m)))
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+            bar.abort()
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for r in range(world):
+        for (s, b), t in stores[r].items():
+            assert np.array_equal(t.cpu().numpy(), ref[s, b]), (r, s, b)
