@@ -132,7 +132,19 @@ def cpu_baseline(c, seconds: float):
         if el >= seconds:
             break
     user = threads * c["k"] * prefix
+    # single thread, one stripe: the paper's per-core framing
+    st1, er1 = oracle_sample(c, 1, prefix)
+    p1, t1 = 0, time.perf_counter()
+    while True:
+        oracle_pass(oracle, st1, er1, c, 1)
+        p1 += 1
+        e1 = time.perf_counter() - t1
+        if e1 >= seconds / 4:
+            break
+    single = {"value": round(2 * c["k"] * prefix * p1 / e1 / 1e9, 4), "unit": "GB/s", "cores": 1,
+              "sample": f"1 stripe x {c['k']} data blocks x first {prefix} B, {p1} passes in {e1:.1f} s"}
     return {"value": round(2 * user * passes / el / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "single_thread": single,
             "sample": f"{threads} stripes x {c['k']} data blocks x first {prefix} B of each block "
                       f"({user / 2**20:.0f} MiB user data), encode + decode with the config's erasure patterns, "
                       f"{passes} passes in {el:.1f} s, {threads} threads (one stripe each) of {cores} host cores"}
