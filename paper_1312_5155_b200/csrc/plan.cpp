@@ -93,7 +93,11 @@ class CompilePool {
     q_.push_back(std::move(fn));
     cv_.notify_one();
   }
+  // True once the process is tearing the pool down: queued jobs then resolve their
+  // promises with a failed kernel instead of compiling (fast exit, no waiter left hanging).
+  static bool stopping() { return stopping_flag().load(); }
   ~CompilePool() {
+    stopping_flag().store(true);
     {
       std::lock_guard<std::mutex> l(mu_);
       stop_ = true;
@@ -119,6 +123,10 @@ class CompilePool {
       }
       fn();
     }
+  }
+  static std::atomic<bool> &stopping_flag() {
+    static std::atomic<bool> f{false};
+    return f;
   }
   std::mutex mu_;
   std::condition_variable cv_;
@@ -452,6 +460,12 @@ const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const JitKey &key, const 
     int dev = 0;
     cudaGetDevice(&dev);
     auto job = [prom, spec = mk(), F = &P.F, dev]() {
+      if (CompilePool::stopping()) {  // process exit: do not compile, do not touch CUDA
+        auto k = std::make_shared<rsb::jit::Kernel>();
+        k->log = "cancelled at exit";
+        prom->set_value(k);
+        return;
+      }
       cudaSetDevice(dev);  // load the module under the caller's device, not device 0
       int xors = 0;
       const std::string src = rsb::jit::source(*F, spec, &xors);
