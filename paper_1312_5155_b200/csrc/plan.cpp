@@ -1034,22 +1034,30 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   std::vector<size_t> grp_off(pats.size(), SIZE_MAX);
   for (size_t i = 0; i < pats.size(); ++i)
     if (!groups[i].empty()) grp_off[i] = b.add(groups[i].data(), sizeof(int32_t) * groups[i].size());
-  std::vector<rsb::SlicedPat> sps(pats.size());
-  std::vector<rsb::GenericPat> gps(pats.size());
+  const bool records = any_rt || body * UB < G.block_bytes;  // a table kernel will run
+  std::vector<rsb::SlicedPat> sps(records ? pats.size() : 0);
+  std::vector<rsb::GenericPat> gps(records ? pats.size() : 0);
   const size_t sliced_pats_off = b.add(nullptr, sizeof(rsb::SlicedPat) * sps.size());
   const size_t generic_pats_off = b.add(nullptr, sizeof(rsb::GenericPat) * gps.size());
   const size_t tables_off = b.add(nullptr, 0);
   uint32_t max_groups = 1, max_in = 1;
-  for (size_t i = 0; i < pats.size(); ++i) {
+  // Table records only for the patterns a table kernel will read: every pattern when there
+  // is a ragged tail, else only those still without a JIT kernel (a many-pattern batch
+  // would otherwise upload ~2 KB of tables per pattern per call for nothing).
+  const bool tail = body * UB < G.block_bytes;
+  for (size_t i = 0; i < sps.size(); ++i) {
     const PatternHost &ph = *pats[i];
-    if (P->sliced) {
+    const bool needs_rt = jk[i] == nullptr && any_rt;
+    if (sliced_rt && needs_rt) {
       sps[i] = ph.sp;
       sps[i].table_off = (uint32_t)(b.add(ph.wtab.data(), ph.wtab.size()) - tables_off);
     }
-    gps[i] = ph.gp;
-    gps[i].table_off = (uint32_t)(b.add(ph.rtab.data(), ph.rtab.size()) - tables_off);
-    max_groups = std::max<uint32_t>(max_groups, (uint32_t)((ph.gp.n_out + 3) / 4));
-    max_in = std::max<uint32_t>(max_in, (uint32_t)ph.gp.n_in);
+    if (tail || (needs_rt && !sliced_rt)) {
+      gps[i] = ph.gp;
+      gps[i].table_off = (uint32_t)(b.add(ph.rtab.data(), ph.rtab.size()) - tables_off);
+      max_groups = std::max<uint32_t>(max_groups, (uint32_t)((ph.gp.n_out + 3) / 4));
+      max_in = std::max<uint32_t>(max_in, (uint32_t)ph.gp.n_in);
+    }
   }
   std::memcpy(b.h.data() + sliced_pats_off, sps.data(), sizeof(rsb::SlicedPat) * sps.size());
   std::memcpy(b.h.data() + generic_pats_off, gps.data(), sizeof(rsb::GenericPat) * gps.size());
