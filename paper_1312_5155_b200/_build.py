@@ -58,8 +58,8 @@ def build(verbose_ptxas: bool = False) -> list[str]:
            "kBitsliceDeviceSrc")
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.inc")) + glob.glob(os.path.join(CSRC, "*.hpp")) + \
         glob.glob(os.path.join(INCLUDE, "*.h"))
-    poly_src = [os.path.join(CSRC, "rs_kernels.cu"), os.path.join(CSRC, "polyrs_ablation.cu"),
-                os.path.join(CSRC, "plan.cpp"), os.path.join(CSRC, "jit.cpp")]
+    poly_src = [os.path.join(CSRC, f) for f in ("rs_kernels.cu", "polyrs_ablation.cu", "plan.cpp", "linear.cpp",
+                                                 "host_pipeline.cpp", "jit.cpp")]
     extra = ["-Xptxas", "-v"] if verbose_ptxas else []
     if _stale(POLY_LIB, poly_src + headers + [__file__]):
         tmp = POLY_LIB + ".tmp%d" % os.getpid()

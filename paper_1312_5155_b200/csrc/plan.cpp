@@ -9,217 +9,10 @@
 //   R = V_E^{-1} A_E,  A_E[j][s] = alpha^{j pos(s)} over survivors s (generic)
 // and the packed split-nibble tables the kernels read.  Both are exact
 // rewritings of y = V_E^{-1} (D(alpha^0..alpha^{t-1})) -- see DESIGN.md.
-#include <algorithm>
-#include <array>
-#include <atomic>
-#include <condition_variable>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <deque>
-#include <functional>
-#include <future>
-#include <map>
-#include <string>
-#include <memory>
-#include <mutex>
-#include <new>
-#include <thread>
-#include <vector>
+#include "plan_internal.hpp"
 
-#include "../../include/rs_poly.h"
-#include "gf.hpp"
-#include "jit.hpp"
-#include "rs_kernels.cuh"
+namespace rsp {
 
-using rsb::Field;
-
-namespace {
-
-struct PatternHost {
-  std::vector<int> erased;  // row order of W / R: ascending API index
-  std::vector<int> surv;    // survivors, ascending API index (columns of R)
-  std::vector<uint32_t> R;  // t x (n-t) decode matrix V_E^{-1} A_E
-  std::vector<uint32_t> Vinv;  // t x t, V_E^{-1} (Step 2)
-  // Syndrome-form (w16 JIT) solve: unknowns U (= E, or E + the survivors not read under
-  // RS_READ_K_SURVIVORS), Hm = rows E of V_U^{-1} (t x |U|), |U| syndromes used.
-  std::vector<int> unknown;
-  std::vector<uint32_t> Hm;
-  rsb::SlicedPat sp{};
-  std::vector<uint8_t> wtab;  // sliced W tables
-  rsb::GenericPat gp{};
-  std::vector<uint8_t> rtab;  // generic R tables (all output groups)
-};
-
-using MaskKey = std::array<uint64_t, 4>;
-// JIT cache key: (kind, mask).  Decode: the erased mask; encode: 0; linear job: its id.
-enum JitKind { kJitDecode = 0, kJitEncode = 1, kJitLinear = 2 };
-using JitKey = std::pair<int, MaskKey>;
-
-// A "linear job": per stripe the kernels see nv virtual blocks (a pointer table) and
-// compute out_r = sum_v M[r][v] in_v for the nout virtual blocks out[r] (which may also
-// be inputs: in place).  Used by the diff-update, the partial encoder of the
-// cross-GPU placement and the XOR reduction.  Cached per plan by a signature string.
-struct LinearHost {
-  int id = 0;               // JIT key
-  int nv = 0, nout = 0;
-  std::vector<int> out;     // virtual indices of the outputs
-  std::vector<uint32_t> M;  // nout x nv
-  int group_blocks = 0;     // JIT CSE group (0 = by field)
-  rsb::GenericPat gp{};
-  std::vector<uint8_t> tab;
-};
-
-// A run-time specialised kernel (jit.cpp), compiled once per pattern.
-struct JitEntry {
-  std::shared_future<std::shared_ptr<rsb::jit::Kernel>> fut;
-  bool ready() const { return fut.valid() && fut.wait_for(std::chrono::seconds(0)) == std::future_status::ready; }
-  const rsb::jit::Kernel *kernel() const {
-    if (!ready()) return nullptr;
-    const auto &k = fut.get();
-    return (k && k->ok) ? k.get() : nullptr;
-  }
-};
-
-// Fixed pool of compile workers shared by all plans (NVRTC is thread-safe).
-class CompilePool {
- public:
-  static CompilePool &get() {
-    static CompilePool p;
-    return p;
-  }
-  void submit(std::function<void()> fn) {
-    std::lock_guard<std::mutex> l(mu_);
-    q_.push_back(std::move(fn));
-    cv_.notify_one();
-  }
-  // True once the process is tearing the pool down: queued jobs then resolve their
-  // promises with a failed kernel instead of compiling (fast exit, no waiter left hanging).
-  static bool stopping() { return stopping_flag().load(); }
-  ~CompilePool() {
-    stopping_flag().store(true);
-    {
-      std::lock_guard<std::mutex> l(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto &t : th_) t.join();
-  }
-
- private:
-  CompilePool() {
-    unsigned n = std::max(2u, std::min(16u, std::thread::hardware_concurrency()));
-    for (unsigned i = 0; i < n; ++i) th_.emplace_back([this] { run(); });
-  }
-  void run() {
-    for (;;) {
-      std::function<void()> fn;
-      {
-        std::unique_lock<std::mutex> l(mu_);
-        cv_.wait(l, [this] { return stop_ || !q_.empty(); });
-        if (q_.empty()) return;
-        fn = std::move(q_.front());
-        q_.pop_front();
-      }
-      fn();
-    }
-  }
-  static std::atomic<bool> &stopping_flag() {
-    static std::atomic<bool> f{false};
-    return f;
-  }
-  std::mutex mu_;
-  std::condition_variable cv_;
-  std::deque<std::function<void()>> q_;
-  std::vector<std::thread> th_;
-  bool stop_ = false;
-};
-
-}  // namespace
-
-struct rs_poly_plan {
-  int k = 0, m = 0, w = 0, n = 0;
-  uint32_t poly = 0;
-  Field F;
-  std::vector<uint32_t> g, pmap;
-  bool sliced = false;
-  rsb::GenericPat enc_gp{};
-  std::vector<uint8_t> enc_tab;
-  mutable std::mutex mu;
-  mutable std::map<MaskKey, std::shared_ptr<const PatternHost>> cache;
-  mutable std::map<std::string, std::shared_ptr<const LinearHost>> lin_cache;  // linear jobs by signature
-  // run-time specialised kernels: decode patterns (key = erased mask) and, for codes
-  // without a compiled network, the encoder (key = kEncodeKey)
-  int jit_mode = RS_JIT_BACKGROUND;
-  int read_policy = RS_READ_ALL_SURVIVORS;
-  mutable std::map<JitKey, std::shared_ptr<JitEntry>> jit;
-  std::vector<std::shared_ptr<JitEntry>> retired;  // dropped by a policy change, released at destroy
-  mutable std::map<int, std::vector<cudaStream_t>> pool;  // device -> side streams for concurrent launches
-  mutable std::atomic<uint64_t> jit_launches{0}, table_launches{0};
-  // pinned host slots for the per-call constant blob: a pageable cudaMemcpyAsync may
-  // wait for the stream, stalling the host between back-to-back calls
-  struct PinnedSlot {
-    uint8_t *p = nullptr;
-    size_t cap = 0;
-    int dev = 0;
-    cudaEvent_t ev = nullptr;
-    bool busy = false;
-    uint64_t seq = 0;  // order of last use
-  };
-  mutable uint64_t stage_seq = 0;
-  mutable std::mutex stage_mu;
-  mutable std::vector<PinnedSlot> stage;
-  // device staging of the host entry points (rs_poly_*_host), one per device, reused
-  // across calls: a fresh stream-ordered allocation per call would be re-mapped each
-  // time the default pool trims at the call's final synchronize
-  struct Staging {
-    std::mutex busy;
-    uint8_t *p = nullptr;
-    size_t cap = 0;
-  };
-  mutable std::map<int, std::unique_ptr<Staging>> staging;
-  mutable std::map<int, uint8_t *> enc_dev;  // device -> encode tail constants
-  ~rs_poly_plan() {
-    for (auto &kv : enc_dev) {
-      int cur = 0;
-      cudaGetDevice(&cur);
-      cudaSetDevice(kv.first);
-      cudaFree(kv.second);
-      cudaSetDevice(cur);
-    }
-    for (auto &kv : staging)
-      if (kv.second->p) {
-        int cur = 0;
-        cudaGetDevice(&cur);
-        cudaSetDevice(kv.first);
-        cudaFree(kv.second->p);
-        cudaSetDevice(cur);
-      }
-    for (auto &sl : stage) {
-      if (sl.ev) {
-        cudaEventSynchronize(sl.ev);
-        cudaEventDestroy(sl.ev);
-      }
-      if (sl.p) cudaFreeHost(sl.p);
-    }
-    for (auto &kv : jit) retired.push_back(kv.second);
-    for (auto &e : retired) {
-      if (e->fut.valid()) {
-        auto k = e->fut.get();
-        if (k) rsb::jit::release(*k);
-      }
-    }
-    for (auto &kv : pool)
-      for (cudaStream_t s : kv.second) cudaStreamDestroy(s);
-  }
-};
-
-namespace {
-
-constexpr int kGenericThreads = 256;
-constexpr int kSlicedThreads = 128;
-constexpr uint32_t kSlicedUnitsPerCta = kSlicedThreads * 8;
-constexpr uint64_t kGenericChunk = 64 * 1024;
 
 // Packed split-nibble tables for "out_r = sum_s M[r][s] in_s" (layout in rs_kernels.cuh).
 void pack_generic_tables(const Field &F, int w, const std::vector<uint32_t> &M, int n_out, int n_in,
@@ -340,29 +133,9 @@ rs_status cuda_status(cudaError_t e) {
   return RS_ERR_CUDA;
 }
 
-// Per-call device blob: uploaded with one H2D copy, freed stream-ordered.
-struct Blob {
-  std::vector<uint8_t> h;
-  size_t add(const void *p, size_t bytes) {
-    size_t off = (h.size() + 15) & ~(size_t)15;
-    h.resize(off + bytes);
-    if (p && bytes) std::memcpy(h.data() + off, p, bytes);
-    return off;
-  }
-};
 
-struct Geometry {
-  rsb::Layout L{};
-  uint64_t n_stripes = 0, block_bytes = 0;
-  bool aligned32 = false, aligned16 = false;
-};
 
-bool ptr_aligned(uint64_t v, uint64_t a) { return (v % a) == 0; }
 
-const JitKey kEncodeKey{kJitEncode, MaskKey{0, 0, 0, 0}};
-// At most this many JIT modules per plan (each is ~50-150 KB of code); RS(10,4) has 1001
-// erasure patterns, RS(12,4) 2516.  Beyond it, new patterns run on the table kernels.
-constexpr size_t kMaxJitKernels = 8192;
 
 bool jit_eligible(const rs_poly_plan &P, int n_out) { return P.w == 8 ? n_out <= 8 : n_out <= 4; }
 
@@ -540,7 +313,7 @@ uint32_t units_per_cta_for(uint64_t total) {
 }
 
 cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32_t *stripes, uint64_t n_sel,
-                       uint64_t body_units, cudaStream_t st, bool pdl = false, uint64_t stripe_base = 0) {
+                       uint64_t body_units, cudaStream_t st, bool pdl, uint64_t stripe_base) {
   rsb::jit::Args a{};
   a.stripe_base = stripe_base;
   a.base = G.L.base;
@@ -667,21 +440,6 @@ cudaError_t upload_pinned(const rs_poly_plan &P, void *dst, const void *src, siz
   return e;
 }
 
-struct DevBlob {
-  uint8_t *p = nullptr;
-  cudaStream_t st = nullptr;
-  cudaError_t upload(const rs_poly_plan &P, const Blob &b, cudaStream_t s) {
-    st = s;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p), std::max<size_t>(b.h.size(), 16), s);
-    if (e != cudaSuccess) return e;
-    return upload_pinned(P, p, b.h.data(), b.h.size(), s);
-  }
-  cudaError_t release() {
-    cudaError_t e = p ? cudaFreeAsync(p, st) : cudaSuccess;
-    p = nullptr;
-    return e;
-  }
-};
 
 rs_status check_geometry(const rs_poly_plan *P, size_t block_bytes) {
   if (!P) return RS_ERR_INVALID_ARG;
@@ -691,7 +449,6 @@ rs_status check_geometry(const rs_poly_plan *P, size_t block_bytes) {
 
 // Device copy of the encode tail constants [GenericPat | tables], made once per plan and
 // device (synchronous upload: later calls on any stream see it).
-constexpr size_t kEncTablesOff = (sizeof(rsb::GenericPat) + 15) & ~(size_t)15;
 const uint8_t *enc_consts(const rs_poly_plan &P) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -787,144 +544,12 @@ rs_status collect_patterns(const rs_poly_plan *P, const std::vector<std::vector<
   return RS_OK;
 }
 
-// ---- linear jobs (diff-update, partial encode, XOR reduction) ----------------
-// Cached LinearHost for `sig`, built by `fill` (which sets nv, out, M, group_blocks).
-std::shared_ptr<const LinearHost> linear_host(const rs_poly_plan &P, const std::string &sig,
-                                              const std::function<void(LinearHost &)> &fill) {
-  std::lock_guard<std::mutex> lock(P.mu);
-  auto it = P.lin_cache.find(sig);
-  if (it != P.lin_cache.end()) return it->second;
-  auto lh = std::make_shared<LinearHost>();
-  fill(*lh);
-  lh->id = (int)P.lin_cache.size() + 1;
-  lh->nout = (int)lh->out.size();
-  std::memset(&lh->gp, 0, sizeof(lh->gp));
-  lh->gp.n_in = lh->nv;
-  lh->gp.n_out = lh->nout;
-  for (int v = 0; v < lh->nv; ++v) lh->gp.in_blk[v] = (uint8_t)v;
-  for (int r = 0; r < lh->nout; ++r) lh->gp.out_blk[r] = (uint8_t)lh->out[r];
-  pack_generic_tables(P.F, P.w, lh->M, lh->nout, lh->nv, lh->tab);
-  P.lin_cache.emplace(sig, lh);
-  return lh;
-}
 
-rsb::jit::Spec linear_spec(const rs_poly_plan &P, const LinearHost &lh) {
-  std::vector<int> in(lh.nv);
-  for (int v = 0; v < lh.nv; ++v) in[v] = v;
-  rsb::jit::Spec s = jit_spec(P, in, lh.out, lh.M);
-  if (lh.group_blocks) s.group_blocks = lh.group_blocks;
-  return s;
-}
 
-// Diff-update of the sorted changed set idx: virtual blocks [new_0, old_0, new_1, old_1, ...,
-// parity_0..m-1]; parity_i <- sum_j P[i][j] (new_j + old_j) + parity_i, M = [P_J P_J | I].
-std::shared_ptr<const LinearHost> update_host(const rs_poly_plan &P, const std::vector<int> &idx) {
-  std::string sig = "U";
-  for (int j : idx) sig += ":" + std::to_string(j);
-  return linear_host(P, sig, [&](LinearHost &lh) {
-    const int c = (int)idx.size(), m = P.m, k = P.k;
-    lh.nv = 2 * c + m;
-    for (int i = 0; i < m; ++i) lh.out.push_back(2 * c + i);
-    lh.M.assign((size_t)m * lh.nv, 0);
-    for (int i = 0; i < m; ++i) {
-      for (int q = 0; q < c; ++q) {
-        const uint32_t coef = P.pmap[(size_t)i * k + idx[q]];  // x^{m+j} mod g, coefficient of x^i
-        lh.M[(size_t)i * lh.nv + 2 * q] = coef;      // new_j
-        lh.M[(size_t)i * lh.nv + 2 * q + 1] = coef;  // old_j (char 2: + = -)
-      }
-      lh.M[(size_t)i * lh.nv + 2 * c + i] = 1;       // the old parity itself
-    }
-    lh.group_blocks = P.w == 8 ? 12 : 4;  // even: each (new_j, old_j) pair shares a CSE group
-  });
-}
 
-// Partial parity of the data subset idx (cross-GPU placement): virtual blocks
-// [d_0..d_{c-1}, partial_0..partial_{m-1}]; partial_i <- sum_j P[i][j] d_j (+ partial_i).
-std::shared_ptr<const LinearHost> partial_host(const rs_poly_plan &P, const std::vector<int> &idx, bool acc) {
-  std::string sig = acc ? "PA" : "P";
-  for (int j : idx) sig += ":" + std::to_string(j);
-  return linear_host(P, sig, [&](LinearHost &lh) {
-    const int c = (int)idx.size(), m = P.m, k = P.k;
-    lh.nv = c + m;
-    for (int i = 0; i < m; ++i) lh.out.push_back(c + i);
-    lh.M.assign((size_t)m * lh.nv, 0);
-    for (int i = 0; i < m; ++i) {
-      for (int q = 0; q < c; ++q) lh.M[(size_t)i * lh.nv + q] = P.pmap[(size_t)i * k + idx[q]];
-      if (acc) lh.M[(size_t)i * lh.nv + c + i] = 1;
-    }
-    lh.group_blocks = P.w == 8 ? 12 : 3;
-  });
-}
 
-// XOR of n_src blocks into one: virtual blocks [src_0..src_{n-1}, dst]; dst <- sum src.
-std::shared_ptr<const LinearHost> xor_host(const rs_poly_plan &P, int n_src) {
-  return linear_host(P, "X:" + std::to_string(n_src), [&](LinearHost &lh) {
-    lh.nv = n_src + 1;
-    lh.out.push_back(n_src);
-    lh.M.assign((size_t)lh.nv, 0);
-    for (int q = 0; q < n_src; ++q) lh.M[q] = 1;  // all pass-through: raw XOR, no transposes
-  });
-}
 
-// ptrs: host [S][nv] virtual block addresses.
-rs_status linear_impl(const rs_poly_plan *P, const LinearHost &lh, const std::vector<uint64_t> &ptrs,
-                      size_t n_stripes, size_t B, cudaStream_t st) {
-  Geometry G;
-  G.L.base = nullptr;
-  G.L.n = lh.nv;
-  G.n_stripes = n_stripes;
-  G.block_bytes = B;
-  G.aligned32 = G.aligned16 = true;
-  for (uint64_t a : ptrs) {
-    G.aligned32 = G.aligned32 && ptr_aligned(a, 32);
-    G.aligned16 = G.aligned16 && ptr_aligned(a, 16);
-  }
-  uint64_t body = body_units_of(*P, G);
-  const rsb::jit::Kernel *jk = nullptr;
-  if (body && jit_eligible(*P, lh.nout))
-    jk = jit_get(*P, JitKey{kJitLinear, MaskKey{(uint64_t)lh.id, 0, 0, 0}}, [&] { return linear_spec(*P, lh); },
-                 false);
-  if (!jk) body = 0;
-  Blob b;
-  const size_t ptrs_off = b.add(ptrs.data(), sizeof(uint64_t) * ptrs.size());
-  rsb::GenericPat gp = lh.gp;
-  gp.table_off = 0;
-  const size_t pats_off = b.add(&gp, sizeof(gp));
-  const size_t tables_off = b.add(lh.tab.data(), lh.tab.size());
-  DevBlob d;
-  cudaError_t e = d.upload(*P, b, st);
-  if (e == cudaSuccess) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
-  if (e == cudaSuccess && body) {
-    e = launch_jit(*jk, G, nullptr, G.n_stripes, body, st);
-    P->jit_launches++;
-  }
-  const uint64_t UB = 32ull * (uint64_t)P->w / 8;
-  if (e == cudaSuccess)
-    e = launch_generic_range(*P, G, body * UB, G.block_bytes, d.p, pats_off, SIZE_MAX, tables_off,
-                             (uint32_t)((lh.nout + 3) / 4), (uint32_t)(lh.nv * (P->w == 8 ? 128 : 512)), st);
-  cudaError_t ef = d.release();
-  return cuda_status(e != cudaSuccess ? e : ef);
-}
 
-// Validates data_idx; returns the permutation sorting it (order[q] = caller position).
-rs_status parse_update(const rs_poly_plan *P, const int *data_idx, int c, std::vector<int> &sorted,
-                       std::vector<int> &order) {
-  sorted.clear();
-  order.clear();
-  if (c < 0 || (c && !data_idx)) return RS_ERR_INVALID_ARG;
-  if (c > P->k) return RS_ERR_BAD_ERASURE;
-  if (2 * c + P->m > RS_POLY_MAX_N) return RS_ERR_INVALID_ARG;
-  std::vector<char> seen(P->k, 0);
-  for (int q = 0; q < c; ++q) {
-    const int j = data_idx[q];
-    if (j < 0 || j >= P->k || seen[j]) return RS_ERR_BAD_ERASURE;
-    seen[j] = 1;
-    order.push_back(q);
-  }
-  std::sort(order.begin(), order.end(), [&](int a, int b2) { return data_idx[a] < data_idx[b2]; });
-  for (int q : order) sorted.push_back(data_idx[q]);
-  return RS_OK;
-}
 
 const rsb::jit::Kernel *pattern_jit(const rs_poly_plan &P, const PatternHost &ph, const MaskKey &key, bool wait) {
   if (!jit_eligible(P, (int)ph.erased.size())) return nullptr;
@@ -1123,7 +748,7 @@ rs_status check_strided(const rs_poly_plan *P, void *stripes, size_t n_stripes, 
   return RS_OK;
 }
 
-}  // namespace
+}  // namespace rsp
 
 // ===========================================================================
 // C ABI
@@ -1254,121 +879,10 @@ size_t rs_poly_jit_source(const rs_poly_plan *P, const int *erasures, int n_eras
   return s.size();
 }
 
-rs_status rs_poly_update(const rs_poly_plan *P, const int *data_idx, int n_changed, const void *const *old_data,
-                         const void *const *new_data, void *const *parity, size_t block_bytes, void *stream) {
-  if (!P) return RS_ERR_INVALID_ARG;
-  std::vector<int> idx, order;
-  rs_status rc = parse_update(P, data_idx, n_changed, idx, order);
-  if (rc) return rc;
-  rc = check_geometry(P, block_bytes);
-  if (rc) return rc;
-  if (n_changed == 0) return RS_OK;
-  if (!old_data || !new_data || !parity) return RS_ERR_INVALID_ARG;
-  const uint64_t a = (uint64_t)(P->w / 8);
-  std::vector<uint64_t> ptrs;
-  for (int q : order) {
-    ptrs.push_back(reinterpret_cast<uint64_t>(new_data[q]));
-    ptrs.push_back(reinterpret_cast<uint64_t>(old_data[q]));
-  }
-  for (int i = 0; i < P->m; ++i) ptrs.push_back(reinterpret_cast<uint64_t>(parity[i]));
-  for (uint64_t v : ptrs)
-    if (!v) return RS_ERR_INVALID_ARG;
-    else if (v % a) return RS_ERR_GEOMETRY;
-  auto uh = update_host(*P, idx);
-  return linear_impl(P, *uh, ptrs, 1, block_bytes, static_cast<cudaStream_t>(stream));
-}
 
-rs_status rs_poly_update_batch(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
-                               size_t block_stride, size_t block_bytes, const int *data_idx, int n_changed,
-                               const void *old_blocks, size_t old_stripe_stride, size_t old_block_stride,
-                               void *stream) {
-  if (!P) return RS_ERR_INVALID_ARG;
-  std::vector<int> idx, order;
-  rs_status rc = parse_update(P, data_idx, n_changed, idx, order);
-  if (rc) return rc;
-  rc = check_strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
-  if (rc) return rc;
-  if (n_changed == 0 || n_stripes == 0) return RS_OK;
-  const uint64_t a = (uint64_t)(P->w / 8);
-  if (!old_blocks) return RS_ERR_INVALID_ARG;
-  if (reinterpret_cast<uint64_t>(old_blocks) % a || old_stripe_stride % a || old_block_stride % a)
-    return RS_ERR_GEOMETRY;
-  if (n_changed > 1 && old_block_stride < block_bytes) return RS_ERR_GEOMETRY;
-  if (n_stripes > 1 && old_stripe_stride < (uint64_t)(n_changed - 1) * old_block_stride + block_bytes)
-    return RS_ERR_GEOMETRY;
-  auto uh = update_host(*P, idx);
-  std::vector<uint64_t> ptrs;
-  ptrs.reserve(n_stripes * (size_t)uh->nv);
-  const uint64_t base = reinterpret_cast<uint64_t>(stripes), obase = reinterpret_cast<uint64_t>(old_blocks);
-  for (size_t s = 0; s < n_stripes; ++s) {
-    for (int q : order) {
-      ptrs.push_back(base + s * stripe_stride + (uint64_t)data_idx[q] * block_stride);
-      ptrs.push_back(obase + s * old_stripe_stride + (uint64_t)q * old_block_stride);
-    }
-    for (int i = 0; i < P->m; ++i) ptrs.push_back(base + s * stripe_stride + (uint64_t)(P->k + i) * block_stride);
-  }
-  return linear_impl(P, *uh, ptrs, n_stripes, block_bytes, static_cast<cudaStream_t>(stream));
-}
 
-rs_status rs_poly_encode_partial(const rs_poly_plan *P, const int *data_idx, int n_data, const void *const *data,
-                                 void *const *partial, size_t n_stripes, size_t block_bytes, int accumulate,
-                                 void *stream) {
-  if (!P) return RS_ERR_INVALID_ARG;
-  std::vector<int> idx, order;
-  rs_status rc = parse_update(P, data_idx, n_data, idx, order);
-  if (rc) return rc;
-  rc = check_geometry(P, block_bytes);
-  if (rc) return rc;
-  if (n_stripes == 0 || (n_data == 0 && accumulate)) return RS_OK;
-  if (!partial || (n_data && !data)) return RS_ERR_INVALID_ARG;
-  const uint64_t a = (uint64_t)(P->w / 8);
-  auto lh = partial_host(*P, idx, accumulate != 0);
-  std::vector<uint64_t> ptrs;
-  ptrs.reserve(n_stripes * (size_t)lh->nv);
-  for (size_t s = 0; s < n_stripes; ++s) {
-    for (int q : order) ptrs.push_back(reinterpret_cast<uint64_t>(data[s * (size_t)n_data + q]));
-    for (int i = 0; i < P->m; ++i) ptrs.push_back(reinterpret_cast<uint64_t>(partial[s * (size_t)P->m + i]));
-  }
-  for (uint64_t v : ptrs)
-    if (!v) return RS_ERR_INVALID_ARG;
-    else if (v % a) return RS_ERR_GEOMETRY;
-  return linear_impl(P, *lh, ptrs, n_stripes, block_bytes, static_cast<cudaStream_t>(stream));
-}
 
-rs_status rs_poly_xor_reduce(const rs_poly_plan *P, void *const *dst, const void *const *srcs, int n_src,
-                             size_t n_stripes, size_t bytes, void *stream) {
-  if (!P || n_src < 1 || n_src + 1 > RS_POLY_MAX_N) return RS_ERR_INVALID_ARG;
-  rs_status rc = check_geometry(P, bytes);
-  if (rc) return rc;
-  if (n_stripes == 0) return RS_OK;
-  if (!dst || !srcs) return RS_ERR_INVALID_ARG;
-  const uint64_t a = (uint64_t)(P->w / 8);
-  auto lh = xor_host(*P, n_src);
-  std::vector<uint64_t> ptrs;
-  ptrs.reserve(n_stripes * (size_t)lh->nv);
-  for (size_t s = 0; s < n_stripes; ++s) {
-    for (int q = 0; q < n_src; ++q) ptrs.push_back(reinterpret_cast<uint64_t>(srcs[s * (size_t)n_src + q]));
-    ptrs.push_back(reinterpret_cast<uint64_t>(dst[s]));
-  }
-  for (uint64_t v : ptrs)
-    if (!v) return RS_ERR_INVALID_ARG;
-    else if (v % a) return RS_ERR_GEOMETRY;
-  return linear_impl(P, *lh, ptrs, n_stripes, bytes, static_cast<cudaStream_t>(stream));
-}
 
-size_t rs_poly_update_jit_source(const rs_poly_plan *P, const int *data_idx, int n_changed, char *buf,
-                                 size_t cap) {
-  if (!P || n_changed < 1 || !jit_eligible(*P, P->m)) return 0;
-  std::vector<int> idx, order;
-  if (parse_update(P, data_idx, n_changed, idx, order)) return 0;
-  const std::string s = rsb::jit::source(P->F, linear_spec(*P, *update_host(*P, idx)), nullptr);
-  if (buf && cap) {
-    const size_t nc = std::min(cap - 1, s.size());
-    std::memcpy(buf, s.data(), nc);
-    buf[nc] = 0;
-  }
-  return s.size();
-}
 
 rs_status rs_poly_ablation_decode(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
                                   size_t block_stride, size_t block_bytes, const int *erasures, int n_erasures,
@@ -1520,148 +1034,3 @@ rs_status rs_poly_decode_batch(const rs_poly_plan *P, void *stripes, size_t n_st
 
 }  // extern "C"
 
-// ===========================================================================
-// End to end from host memory: chunks of stripes stream through device
-// staging buffers, H2D -> kernels -> D2H, overlapped over kNumLanes streams.
-// ===========================================================================
-namespace {
-
-constexpr int kNumLanes = 3;
-constexpr uint64_t kStagingTarget = 256ull << 20;  // bytes of staging per lane
-
-rs_status host_impl(const rs_poly_plan *P, bool decode, uint8_t *host, size_t n_stripes, size_t ss, size_t bs,
-                    size_t B, const int32_t *erasures, cudaStream_t user, uint64_t *h2d, uint64_t *d2h) {
-  rs_status rc = check_strided(P, host, n_stripes, ss, bs, B);
-  if (rc) return rc;
-  std::vector<std::vector<int>> rows;
-  if (decode) {
-    if (!erasures) return RS_ERR_INVALID_ARG;
-    rows.resize(n_stripes);
-    for (size_t s = 0; s < n_stripes; ++s) {
-      rc = parse_row(P, erasures + s * (size_t)P->m, P->m, rows[s], true);
-      if (rc) return rc;
-    }
-  }
-  uint64_t in_bytes = 0, out_bytes = 0;
-  if (n_stripes == 0) {
-    if (h2d) *h2d = 0;
-    if (d2h) *d2h = 0;
-    return RS_OK;
-  }
-  const int n = P->n;
-  const uint64_t Bp = (B + 255) & ~255ull;  // device block pitch (32-byte aligned for the sliced path)
-  const uint64_t stripe_dev = Bp * (uint64_t)n;
-  const uint64_t per_chunk = std::max<uint64_t>(1, kStagingTarget / stripe_dev);
-  cudaStream_t lanes[kNumLanes] = {};
-  uint8_t *stage[kNumLanes] = {};
-  bool owned_async = false;  // staging from cudaMallocAsync (plan staging busy in another call)
-  cudaEvent_t start = nullptr;
-  cudaError_t e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventRecord(start, user);
-  const size_t lane_bytes = per_chunk * stripe_dev;
-  rs_poly_plan::Staging *sg = nullptr;
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lock(P->mu);
-    auto &slot = P->staging[dev];
-    if (!slot) slot = std::make_unique<rs_poly_plan::Staging>();
-    if (slot->busy.try_lock()) sg = slot.get();
-  }
-  if (sg && e == cudaSuccess && sg->cap < lane_bytes * kNumLanes) {
-    if (sg->p) cudaFree(sg->p);  // idle: its last user synchronized before releasing it
-    sg->p = nullptr;
-    sg->cap = 0;
-    e = cudaMalloc(reinterpret_cast<void **>(&sg->p), lane_bytes * kNumLanes);
-    if (e == cudaSuccess) sg->cap = lane_bytes * kNumLanes;
-  }
-  owned_async = sg == nullptr;
-  for (int l = 0; l < kNumLanes && e == cudaSuccess; ++l) {
-    e = cudaStreamCreateWithFlags(&lanes[l], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(lanes[l], start, 0);
-    if (e != cudaSuccess) break;
-    if (owned_async) e = cudaMallocAsync(reinterpret_cast<void **>(&stage[l]), lane_bytes, lanes[l]);
-    else stage[l] = sg->p + (size_t)l * lane_bytes;
-  }
-  rc = cuda_status(e);
-  for (size_t s0 = 0, ci = 0; rc == RS_OK && s0 < n_stripes; s0 += per_chunk, ++ci) {
-    const size_t cnt = std::min<size_t>(per_chunk, n_stripes - s0);
-    const int l = (int)(ci % kNumLanes);
-    cudaStream_t st = lanes[l];
-    // inputs host -> device
-    for (size_t s = s0; s < s0 + cnt && e == cudaSuccess; ++s) {
-      uint8_t *hs = host + s * ss, *ds = stage[l] + (s - s0) * stripe_dev;
-      if (!decode) {
-        e = cudaMemcpy2DAsync(ds, Bp, hs, bs, B, (size_t)P->k, cudaMemcpyHostToDevice, st);
-        in_bytes += (uint64_t)P->k * B;
-      } else {
-        std::vector<char> er(n, 0);
-        for (int b : rows[s]) er[b] = 1;
-        if (rows[s].empty()) continue;
-        for (int b = 0; b < n && e == cudaSuccess; ++b)
-          if (!er[b]) {
-            e = cudaMemcpyAsync(ds + b * Bp, hs + b * bs, B, cudaMemcpyHostToDevice, st);
-            in_bytes += B;
-          }
-      }
-    }
-    if (e != cudaSuccess) { rc = cuda_status(e); break; }
-    Geometry G = strided(P, stage[l], cnt, stripe_dev, Bp, B);
-    if (!decode) {
-      rc = encode_impl(P, G, nullptr, st);
-    } else {
-      std::vector<std::vector<int>> sub(rows.begin() + s0, rows.begin() + s0 + cnt);
-      rc = decode_impl(P, G, nullptr, sub, st);
-    }
-    if (rc) break;
-    // outputs device -> host
-    for (size_t s = s0; s < s0 + cnt && e == cudaSuccess; ++s) {
-      uint8_t *hs = host + s * ss, *ds = stage[l] + (s - s0) * stripe_dev;
-      if (!decode) {
-        e = cudaMemcpy2DAsync(hs + (size_t)P->k * bs, bs, ds + (size_t)P->k * Bp, Bp, B, (size_t)P->m,
-                              cudaMemcpyDeviceToHost, st);
-        out_bytes += (uint64_t)P->m * B;
-      } else {
-        for (int b : rows[s]) {
-          if (e != cudaSuccess) break;
-          e = cudaMemcpyAsync(hs + b * bs, ds + b * Bp, B, cudaMemcpyDeviceToHost, st);
-          out_bytes += B;
-        }
-      }
-    }
-    if (e != cudaSuccess) rc = cuda_status(e);
-  }
-  for (int l = 0; l < kNumLanes; ++l) {
-    if (stage[l] && owned_async) cudaFreeAsync(stage[l], lanes[l]);
-    if (lanes[l]) {
-      cudaError_t es = cudaStreamSynchronize(lanes[l]);
-      if (rc == RS_OK && es != cudaSuccess) rc = cuda_status(es);
-      cudaStreamDestroy(lanes[l]);
-    }
-  }
-  if (sg) sg->busy.unlock();
-  if (start) cudaEventDestroy(start);
-  if (h2d) *h2d = in_bytes;
-  if (d2h) *d2h = out_bytes;
-  return rc;
-}
-
-}  // namespace
-
-extern "C" {
-
-rs_status rs_poly_encode_host(const rs_poly_plan *P, void *host_stripes, size_t n_stripes, size_t stripe_stride,
-                              size_t block_stride, size_t block_bytes, void *stream, uint64_t *h2d_bytes,
-                              uint64_t *d2h_bytes) {
-  return host_impl(P, false, static_cast<uint8_t *>(host_stripes), n_stripes, stripe_stride, block_stride,
-                   block_bytes, nullptr, static_cast<cudaStream_t>(stream), h2d_bytes, d2h_bytes);
-}
-
-rs_status rs_poly_decode_host(const rs_poly_plan *P, void *host_stripes, size_t n_stripes, size_t stripe_stride,
-                              size_t block_stride, size_t block_bytes, const int32_t *erasures, void *stream,
-                              uint64_t *h2d_bytes, uint64_t *d2h_bytes) {
-  return host_impl(P, true, static_cast<uint8_t *>(host_stripes), n_stripes, stripe_stride, block_stride,
-                   block_bytes, erasures, static_cast<cudaStream_t>(stream), h2d_bytes, d2h_bytes);
-}
-
-}  // extern "C"
