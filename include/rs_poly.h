@@ -111,6 +111,17 @@ rs_status rs_poly_decode_batch(const rs_poly_plan *plan, void *stripes, size_t n
                                size_t stripe_stride, size_t block_stride, size_t block_bytes,
                                const int32_t *erasures, void *stream);
 
+/* ---- verify (scrub) -----------------------------------------------------------
+ * Every codeword vanishes at the roots alpha^0..alpha^{m-1} of g: its m
+ * syndromes S_j = sum_p c_p alpha^{j*pos(p)} (Step 1 of the decode, with
+ * nothing erased) are zero.  For each stripe of the batch (layout as in
+ * rs_poly_encode_batch; nothing is written to it) sets flags[s] = 0 if every column is a
+ * codeword, 1 otherwise (silent corruption of any data or parity byte).  flags: DEVICE
+ * array of n_stripes uint32, overwritten.  Reads n*B bytes per stripe. */
+rs_status rs_poly_verify_batch(const rs_poly_plan *plan, const void *stripes, size_t n_stripes,
+                               size_t stripe_stride, size_t block_stride, size_t block_bytes,
+                               unsigned *flags, void *stream);
+
 /* ---- end to end from HOST memory ---------------------------------------------
  * Same operations, but `host_stripes` is HOST memory (page-locked for full
  * speed, e.g. cudaHostAlloc / torch pin_memory), laid out as in the batched

@@ -38,6 +38,9 @@ struct Spec {
   // 0: straight-line code with the erased set compiled in
   int loop_unroll = 0;
   int pos_top = 0, k = 0, m = 0;
+  // verify: compute the outputs (syndromes) but, instead of storing them, flag the stripe
+  // (Args::flags[s] |= 1) when any is non-zero
+  bool verify = false;
 };
 
 struct Kernel {
@@ -61,6 +64,7 @@ struct Args {
   uint64_t n_sel, units_per_stripe;
   uint32_t units_per_cta, ctas_per_stripe;
   uint64_t stripe_base;
+  unsigned *flags;  // verify kernels: per stripe, set to 1 if not a codeword
 };
 
 bool available(std::string *why = nullptr);

@@ -313,9 +313,10 @@ uint32_t units_per_cta_for(uint64_t total) {
 }
 
 cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32_t *stripes, uint64_t n_sel,
-                       uint64_t body_units, cudaStream_t st, bool pdl, uint64_t stripe_base) {
+                       uint64_t body_units, cudaStream_t st, bool pdl, uint64_t stripe_base, unsigned *flags) {
   rsb::jit::Args a{};
   a.stripe_base = stripe_base;
+  a.flags = flags;
   a.base = G.L.base;
   a.stripe_stride = G.L.stripe_stride;
   a.block_stride = G.L.block_stride;
@@ -367,9 +368,10 @@ cudaError_t launch_sliced_body(const rs_poly_plan &P, bool decode, const Geometr
 
 cudaError_t launch_generic_range(const rs_poly_plan &P, const Geometry &G, uint64_t col_begin, uint64_t col_end,
                                  const uint8_t *dev, size_t pats_off, size_t idx_off, size_t tables_off,
-                                 uint32_t groups, uint32_t smem, cudaStream_t st) {
+                                 uint32_t groups, uint32_t smem, cudaStream_t st, unsigned *flags) {
   if (col_begin >= col_end) return cudaSuccess;
   rsb::GenericArgs a{};
+  a.flags = flags;
   a.L = G.L;
   a.pats = reinterpret_cast<const rsb::GenericPat *>(dev + pats_off);
   a.pat_idx = idx_off == SIZE_MAX ? nullptr : reinterpret_cast<const int32_t *>(dev + idx_off);
@@ -748,6 +750,81 @@ rs_status check_strided(const rs_poly_plan *P, void *stripes, size_t n_stripes, 
   return RS_OK;
 }
 
+// ---- verify (scrub): are the stripes codewords? -----------------------------
+// Every codeword vanishes at the roots alpha^0..alpha^{m-1} of g, i.e. its m
+// syndromes S_j = sum_p c_p alpha^{j p} (Step 1 of the decode, with nothing
+// erased) are zero; a stripe with any non-zero syndrome in any column is flagged.
+rsb::jit::Spec verify_spec(const rs_poly_plan &P) {
+  const int n = P.n, m = P.m;
+  std::vector<int> in(n), out(m);
+  for (int b = 0; b < n; ++b) in[b] = b;
+  for (int i = 0; i < m; ++i) out[i] = i;  // nothing is stored in verify mode
+  std::vector<uint32_t> A((size_t)m * n);
+  for (int j = 0; j < m; ++j)
+    for (int b = 0; b < n; ++b)
+      A[(size_t)j * n + b] = P.F.alpha_pow((uint64_t)j * (uint64_t)rsb::position(b, P.k, m));
+  rsb::jit::Spec s = jit_spec(P, in, out, A);
+  s.verify = true;
+  if (P.w == 16) {
+    s.horner = true;
+    s.poly = P.poly;
+    s.T = m;
+    for (int pos = n - 1; pos >= 0; --pos) s.seq.push_back(pos >= m ? pos - m : P.k + pos);
+    s.min_blocks = 3;
+  } else {
+    s.group_blocks = 10;  // n * 8 input planes in CSE groups of 10 blocks
+  }
+  return s;
+}
+
+// Device copy of [GenericPat | tables] for the syndrome map A (m x n), once per plan and device.
+const uint8_t *ver_consts(const rs_poly_plan &P) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(P.mu);
+  auto it = P.ver_dev.find(dev);
+  if (it != P.ver_dev.end()) return it->second;
+  const rsb::jit::Spec sp = verify_spec(P);
+  std::vector<uint8_t> tab;
+  pack_generic_tables(P.F, P.w, sp.M, P.m, P.n, tab);
+  rsb::GenericPat gp;
+  std::memset(&gp, 0, sizeof(gp));
+  gp.n_in = P.n;
+  gp.n_out = P.m;
+  for (int b = 0; b < P.n; ++b) gp.in_blk[b] = (uint8_t)b;
+  std::vector<uint8_t> h(kEncTablesOff + tab.size(), 0);
+  std::memcpy(h.data(), &gp, sizeof(gp));
+  std::memcpy(h.data() + kEncTablesOff, tab.data(), tab.size());
+  uint8_t *d = nullptr;
+  if (cudaMalloc(reinterpret_cast<void **>(&d), h.size()) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  P.ver_dev.emplace(dev, d);
+  return d;
+}
+
+rs_status verify_impl(const rs_poly_plan *P, Geometry G, unsigned *flags, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned) * G.n_stripes, st);
+  uint64_t body = body_units_of(*P, G);
+  const rsb::jit::Kernel *jk = nullptr;
+  if (body && e == cudaSuccess && jit_eligible(*P, P->m))
+    jk = jit_get(*P, JitKey{kJitVerify, MaskKey{0, 0, 0, 0}}, [&] { return verify_spec(*P); }, false);
+  if (!jk) body = 0;
+  const uint64_t UB = 32ull * (uint64_t)P->w / 8;
+  const uint8_t *cdev = nullptr;
+  if (e == cudaSuccess && body * UB < G.block_bytes && !(cdev = ver_consts(*P))) return RS_ERR_CUDA;
+  if (e == cudaSuccess && body) {
+    e = launch_jit(*jk, G, nullptr, G.n_stripes, body, st, false, 0, flags);
+    P->jit_launches++;
+  }
+  if (e == cudaSuccess)
+    e = launch_generic_range(*P, G, body * UB, G.block_bytes, cdev, 0, SIZE_MAX, kEncTablesOff,
+                             (uint32_t)((P->m + 3) / 4), (uint32_t)(P->n * (P->w == 8 ? 128 : 512)), st, flags);
+  return cuda_status(e);
+}
+
 }  // namespace rsp
 
 // ===========================================================================
@@ -921,6 +998,16 @@ rs_status rs_poly_ablation_decode(const rs_poly_plan *P, void *stripes, size_t n
                                     sm_count(), st);
   cudaError_t ef = d.release();
   return cuda_status(e != cudaSuccess ? e : ef);
+}
+
+rs_status rs_poly_verify_batch(const rs_poly_plan *P, const void *stripes, size_t n_stripes, size_t stripe_stride,
+                               size_t block_stride, size_t block_bytes, unsigned *flags, void *stream) {
+  rs_status rc = check_strided(P, const_cast<void *>(stripes), n_stripes, stripe_stride, block_stride, block_bytes);
+  if (rc) return rc;
+  if (n_stripes == 0) return RS_OK;
+  if (!flags) return RS_ERR_INVALID_ARG;
+  return verify_impl(P, strided(P, const_cast<void *>(stripes), n_stripes, stripe_stride, block_stride, block_bytes),
+                     flags, static_cast<cudaStream_t>(stream));
 }
 
 rs_status rs_poly_plan_stats(const rs_poly_plan *P, rs_poly_stats *out) {

@@ -45,7 +45,7 @@ struct PatternHost {
 
 using MaskKey = std::array<uint64_t, 4>;
 // JIT cache key: (kind, mask).  Decode: the erased mask; encode: 0; linear job: its id.
-enum JitKind { kJitDecode = 0, kJitEncode = 1, kJitLinear = 2 };
+enum JitKind { kJitDecode = 0, kJitEncode = 1, kJitLinear = 2, kJitVerify = 3 };
 using JitKey = std::pair<int, MaskKey>;
 
 // A "linear job": per stripe the kernels see nv virtual blocks (a pointer table) and
@@ -173,14 +173,16 @@ struct rs_poly_plan {
   };
   mutable std::map<int, std::unique_ptr<Staging>> staging;
   mutable std::map<int, uint8_t *> enc_dev;  // device -> encode tail constants
+  mutable std::map<int, uint8_t *> ver_dev;  // device -> verify constants (A = alpha^{j pos})
   ~rs_poly_plan() {
-    for (auto &kv : enc_dev) {
-      int cur = 0;
-      cudaGetDevice(&cur);
-      cudaSetDevice(kv.first);
-      cudaFree(kv.second);
-      cudaSetDevice(cur);
-    }
+    for (auto *mp : {&enc_dev, &ver_dev})
+      for (auto &kv : *mp) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(kv.first);
+        cudaFree(kv.second);
+        cudaSetDevice(cur);
+      }
     for (auto &kv : staging)
       if (kv.second->p) {
         int cur = 0;
@@ -273,13 +275,14 @@ uint64_t body_units_of(const rs_poly_plan &P, const Geometry &G);
 int sm_count();
 uint32_t units_per_cta_for(uint64_t total);
 cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32_t *stripes, uint64_t n_sel,
-                       uint64_t body_units, cudaStream_t st, bool pdl = false, uint64_t stripe_base = 0);
+                       uint64_t body_units, cudaStream_t st, bool pdl = false, uint64_t stripe_base = 0,
+                       unsigned *flags = nullptr);
 cudaError_t launch_sliced_body(const rs_poly_plan &P, bool decode, const Geometry &G, uint64_t body_units,
                                const uint8_t *dev, size_t pats_off, size_t idx_off, size_t tables_off,
                                cudaStream_t st);
 cudaError_t launch_generic_range(const rs_poly_plan &P, const Geometry &G, uint64_t col_begin, uint64_t col_end,
                                  const uint8_t *dev, size_t pats_off, size_t idx_off, size_t tables_off,
-                                 uint32_t groups, uint32_t smem, cudaStream_t st);
+                                 uint32_t groups, uint32_t smem, cudaStream_t st, unsigned *flags = nullptr);
 cudaError_t upload_pinned(const rs_poly_plan &P, void *dst, const void *src, size_t bytes, cudaStream_t s);
 rs_status check_geometry(const rs_poly_plan *P, size_t block_bytes);
 rs_status check_strided(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t ss, size_t bs, size_t B);

@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(con
 // ---------------------------------------------------------------------------
 // generic split-nibble kernel
 // ---------------------------------------------------------------------------
-template <int W>
+// VERIFY: the outputs are syndromes; nothing is stored, a non-zero one sets a.flags[s].
+template <int W, bool VERIFY>
 __global__ void __launch_bounds__(256) generic_kernel(const GenericArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint8_t in_blk[kMaxN + 1];
@@ -318,6 +319,13 @@ __global__ void __launch_bounds__(256) generic_kernel(const GenericArgs a) {
               acc[4 * q + r] ^= T[byte & 15u] ^ T[16 + (byte >> 4)];
             }
         }
+        if (VERIFY) {
+          uint32_t bad = 0;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) bad |= acc[q];
+          if (bad) atomicOr(&a.flags[s], 1u);
+          continue;
+        }
         for (int r = 0; r < nr; ++r) {
           uint32_t o[4];
 #pragma unroll
@@ -343,6 +351,13 @@ __global__ void __launch_bounds__(256) generic_kernel(const GenericArgs a) {
             acc[q].y ^= e0.y ^ e1.y ^ e2.y ^ e3.y;
           }
         }
+        if (VERIFY) {
+          uint32_t bad = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) bad |= acc[q].x | acc[q].y;
+          if (bad) atomicOr(&a.flags[s], 1u);
+          continue;
+        }
         for (int r = 0; r < nr; ++r) {
           uint32_t o[4];
 #pragma unroll
@@ -364,6 +379,10 @@ __global__ void __launch_bounds__(256) generic_kernel(const GenericArgs a) {
             const uint32_t byte = a.L.block(s, in_blk[si])[x];
             acc ^= T32[si * 32 + (byte & 15u)] ^ T32[si * 32 + 16 + (byte >> 4)];
           }
+          if (VERIFY) {
+            if (acc) atomicOr(&a.flags[s], 1u);
+            continue;
+          }
           for (int r = 0; r < nr; ++r) a.L.block(s, out_blk[r])[x] = (uint8_t)(acc >> (8 * r));
         } else {
           uint2 acc = make_uint2(0, 0);
@@ -375,6 +394,10 @@ __global__ void __launch_bounds__(256) generic_kernel(const GenericArgs a) {
             const uint2 e2 = T[32 + ((sym >> 8) & 15u)], e3 = T[48 + (sym >> 12)];
             acc.x ^= e0.x ^ e1.x ^ e2.x ^ e3.x;
             acc.y ^= e0.y ^ e1.y ^ e2.y ^ e3.y;
+          }
+          if (VERIFY) {
+            if (acc.x | acc.y) atomicOr(&a.flags[s], 1u);
+            continue;
           }
           for (int r = 0; r < nr; ++r) {
             const uint32_t v = ((r < 2 ? acc.x : acc.y) >> (16 * (r & 1))) & 0xFFFFu;
@@ -396,16 +419,25 @@ cudaError_t launch_generic(int w, const GenericArgs &a, cudaStream_t st) {
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
   count_launch();
+  const bool verify = a.flags != nullptr;
   if (w == 8) {
-    static bool attr8 = (cudaFuncSetAttribute(generic_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool attr8 = (cudaFuncSetAttribute(generic_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              kMaxN * 128) == cudaSuccess) &&
+                        (cudaFuncSetAttribute(generic_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               kMaxN * 128) == cudaSuccess);
     (void)attr8;
-    generic_kernel<8><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
+    if (verify) generic_kernel<8, true><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
+    else generic_kernel<8, false><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
   } else {
-    static bool attr16 = (cudaFuncSetAttribute(generic_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               kMaxN * 512) == cudaSuccess);
+    static bool attr16 = (cudaFuncSetAttribute(generic_kernel<16, false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxN * 512) ==
+                          cudaSuccess) &&
+                         (cudaFuncSetAttribute(generic_kernel<16, true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxN * 512) ==
+                          cudaSuccess);
     (void)attr16;
-    generic_kernel<16><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
+    if (verify) generic_kernel<16, true><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
+    else generic_kernel<16, false><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
   }
   return cudaGetLastError();
 }

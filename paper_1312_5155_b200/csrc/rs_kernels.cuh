@@ -48,6 +48,7 @@ struct GenericArgs {
   uint32_t n_groups;            // output groups of 4 (max over patterns)
   uint32_t vec_ok;              // all block addresses 16-byte aligned
   uint32_t smem_bytes;          // dynamic smem = table bytes per group
+  unsigned *flags;              // non-null: verify mode (outputs are syndromes; flags[s] |= 1 if any != 0)
 };
 
 // ---- bit-sliced kernels (compile-time networks) ---------------------------

@@ -50,6 +50,7 @@ _lib.rs_poly_update_jit_source.restype = _sz
 _lib.rs_poly_ablation_decode.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _i32, _i32, _vp]
 _lib.rs_poly_encode_partial.argtypes = [_vp, _vp, _i32, _vp, _vp, _sz, _sz, _i32, _vp]
 _lib.rs_poly_xor_reduce.argtypes = [_vp, _vp, _vp, _i32, _sz, _sz, _vp]
+_lib.rs_poly_verify_batch.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _vp]
 
 
 class Stats(ctypes.Structure):
@@ -287,6 +288,14 @@ class Plan:
         e = (ctypes.c_int * max(1, len(er)))(*er)
         _check(_lib.rs_poly_ablation_decode(self._h, ptr, S, ss, bs, B, e, len(er), opt_mask, _stream(stream)),
                "rs_poly_ablation_decode")
+
+    def verify_batch(self, stripes, flags, stream=None) -> None:
+        """flags[s] = 0 if every column of stripe s is a codeword, else 1 (flags: int32 device [S])."""
+        ptr, S, ss, bs, B = _geometry(stripes, self.n)
+        if tuple(flags.shape) != (S,) or flags.element_size() != 4:
+            raise ValueError(f"flags must be a 32-bit device tensor [{S}]")
+        _check(_lib.rs_poly_verify_batch(self._h, ptr, S, ss, bs, B, _ptr(flags), _stream(stream)),
+               "rs_poly_verify_batch")
 
     # ---- end to end from host memory --------------------------------------------
     def encode_host(self, host_stripes, stream=None):

@@ -389,9 +389,47 @@ def run_configs(a):
 
 
 # ---------------------------------------------------------------------------------------
+# verify (scrub): syndromes at the roots of g must vanish
+# ---------------------------------------------------------------------------------------
+def run_verify(a):
+    import torch
+    import paper_1312_5155_b200 as rsp
+    peak, _ = bench.hbm_peak()
+    bad_total = 0
+    for cfg in ("C5", "C3", "C4"):
+        c = dict(synth.CONFIGS[cfg])
+        k, m, w, B, S = c["k"], c["m"], c["w"], c["block_bytes"], c["stripes"]
+        plan = rsp.Plan(k, m, w, c["poly"])
+        plan.set_jit(rsp.RS_JIT_SYNC)
+        st = torch.empty((S, k + m, B), dtype=torch.uint8, device="cuda")
+        rsp.synth_fill(st, k, seed=0)
+        plan.encode_batch(st)
+        flags = torch.empty(S, dtype=torch.int32, device="cuda")
+        plan.verify_batch(st, flags)
+        torch.cuda.synchronize()
+        ok = int(flags.sum().item()) == 0
+        st[S // 2, k + m - 1, B // 3] ^= 0x10          # one flipped bit in one parity block
+        plan.verify_batch(st, flags)
+        torch.cuda.synchronize()
+        ok = ok and flags.nonzero().flatten().tolist() == [S // 2]
+        st[S // 2, k + m - 1, B // 3] ^= 0x10
+        bad_total += 0 if ok else 1
+        ms = statistics.median(timed(lambda: plan.verify_batch(st, flags), a.steps, a.warmup,
+                                     torch.cuda.current_stream()))
+        moved = S * (k + m) * B
+        print(json.dumps({"row": "verify (scrub)", "config": cfg, "k": k, "m": m, "w": w, "stripes": S,
+                          "block_bytes": B, "ms": round(ms, 4), "gbs_read": round(moved / ms / 1e6, 1),
+                          "hbm_frac": round(moved / ms / 1e6 / peak, 4),
+                          "verified": {"clean_batch_all_zero_and_one_flip_flagged": ok}}), flush=True)
+        del st
+        torch.cuda.empty_cache()
+    return 0 if bad_total == 0 else 1
+
+
+# ---------------------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["update", "sweep", "ablation", "placement", "configs"])
+    ap.add_argument("what", choices=["update", "sweep", "ablation", "placement", "configs", "verify"])
     ap.add_argument("--world", type=int, default=8, help="placement: ranks of the emulated layout")
     ap.add_argument("--data-gib", type=int, default=20, help="sweep: user data per point")
     ap.add_argument("--config", default="C5")
@@ -409,6 +447,8 @@ def main():
         return run_placement(a)
     if a.what == "configs":
         return run_configs(a)
+    if a.what == "verify":
+        return run_verify(a)
     return 2
 
 
