@@ -135,6 +135,7 @@ extern "C" {
 rs_status rs_poly_encode_host(const rs_poly_plan *P, void *host_stripes, size_t n_stripes, size_t stripe_stride,
                               size_t block_stride, size_t block_bytes, void *stream, uint64_t *h2d_bytes,
                               uint64_t *d2h_bytes) {
+  NvtxRange nvtx_("rs_poly_encode_host");
   return host_impl(P, false, static_cast<uint8_t *>(host_stripes), n_stripes, stripe_stride, block_stride,
                    block_bytes, nullptr, static_cast<cudaStream_t>(stream), h2d_bytes, d2h_bytes);
 }
@@ -142,6 +143,7 @@ rs_status rs_poly_encode_host(const rs_poly_plan *P, void *host_stripes, size_t 
 rs_status rs_poly_decode_host(const rs_poly_plan *P, void *host_stripes, size_t n_stripes, size_t stripe_stride,
                               size_t block_stride, size_t block_bytes, const int32_t *erasures, void *stream,
                               uint64_t *h2d_bytes, uint64_t *d2h_bytes) {
+  NvtxRange nvtx_("rs_poly_decode_host");
   return host_impl(P, true, static_cast<uint8_t *>(host_stripes), n_stripes, stripe_stride, block_stride,
                    block_bytes, erasures, static_cast<cudaStream_t>(stream), h2d_bytes, d2h_bytes);
 }

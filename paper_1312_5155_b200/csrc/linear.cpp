@@ -153,6 +153,7 @@ extern "C" {
 
 rs_status rs_poly_update(const rs_poly_plan *P, const int *data_idx, int n_changed, const void *const *old_data,
                          const void *const *new_data, void *const *parity, size_t block_bytes, void *stream) {
+  NvtxRange nvtx_("rs_poly_update");
   if (!P) return RS_ERR_INVALID_ARG;
   std::vector<int> idx, order;
   rs_status rc = parse_update(P, data_idx, n_changed, idx, order);
@@ -179,6 +180,7 @@ rs_status rs_poly_update_batch(const rs_poly_plan *P, void *stripes, size_t n_st
                                size_t block_stride, size_t block_bytes, const int *data_idx, int n_changed,
                                const void *old_blocks, size_t old_stripe_stride, size_t old_block_stride,
                                void *stream) {
+  NvtxRange nvtx_("rs_poly_update_batch");
   if (!P) return RS_ERR_INVALID_ARG;
   std::vector<int> idx, order;
   rs_status rc = parse_update(P, data_idx, n_changed, idx, order);
@@ -210,6 +212,7 @@ rs_status rs_poly_update_batch(const rs_poly_plan *P, void *stripes, size_t n_st
 rs_status rs_poly_encode_partial(const rs_poly_plan *P, const int *data_idx, int n_data, const void *const *data,
                                  void *const *partial, size_t n_stripes, size_t block_bytes, int accumulate,
                                  void *stream) {
+  NvtxRange nvtx_("rs_poly_encode_partial");
   if (!P) return RS_ERR_INVALID_ARG;
   std::vector<int> idx, order;
   rs_status rc = parse_update(P, data_idx, n_data, idx, order);
@@ -234,6 +237,7 @@ rs_status rs_poly_encode_partial(const rs_poly_plan *P, const int *data_idx, int
 
 rs_status rs_poly_xor_reduce(const rs_poly_plan *P, void *const *dst, const void *const *srcs, int n_src,
                              size_t n_stripes, size_t bytes, void *stream) {
+  NvtxRange nvtx_("rs_poly_xor_reduce");
   if (!P || n_src < 1 || n_src + 1 > RS_POLY_MAX_N) return RS_ERR_INVALID_ARG;
   rs_status rc = check_geometry(P, bytes);
   if (rc) return rc;

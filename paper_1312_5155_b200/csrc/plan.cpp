@@ -901,6 +901,7 @@ rs_status rs_poly_plan_set_read_policy(rs_poly_plan *P, int policy) {
 }
 
 rs_status rs_poly_prepare(const rs_poly_plan *P, const int32_t *erasures, size_t n_rows) {
+  NvtxRange nvtx_("rs_poly_prepare");
   if (!P || (n_rows && !erasures)) return RS_ERR_INVALID_ARG;
   std::vector<std::vector<int>> rows(n_rows);
   for (size_t s = 0; s < n_rows; ++s) {
@@ -964,6 +965,7 @@ size_t rs_poly_jit_source(const rs_poly_plan *P, const int *erasures, int n_eras
 rs_status rs_poly_ablation_decode(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
                                   size_t block_stride, size_t block_bytes, const int *erasures, int n_erasures,
                                   int opt_mask, void *stream) {
+  NvtxRange nvtx_("rs_poly_ablation_decode");
   if (!P || P->w != 8 || P->n > 32 || n_erasures < 1 || n_erasures > std::min(P->m, 8) || !erasures ||
       opt_mask < 0 || opt_mask > 7)
     return RS_ERR_INVALID_ARG;
@@ -1002,6 +1004,7 @@ rs_status rs_poly_ablation_decode(const rs_poly_plan *P, void *stripes, size_t n
 
 rs_status rs_poly_verify_batch(const rs_poly_plan *P, const void *stripes, size_t n_stripes, size_t stripe_stride,
                                size_t block_stride, size_t block_bytes, unsigned *flags, void *stream) {
+  NvtxRange nvtx_("rs_poly_verify_batch");
   rs_status rc = check_strided(P, const_cast<void *>(stripes), n_stripes, stripe_stride, block_stride, block_bytes);
   if (rc) return rc;
   if (n_stripes == 0) return RS_OK;
@@ -1042,6 +1045,7 @@ int rs_poly_plan_kernel_kind(const rs_poly_plan *P) { return P && P->sliced ? 1 
 
 rs_status rs_poly_encode(const rs_poly_plan *P, const void *const *data, void *const *parity, size_t block_bytes,
                          void *stream) {
+  NvtxRange nvtx_("rs_poly_encode");
   rs_status rc = check_geometry(P, block_bytes);
   if (rc) return rc;
   if (!data || !parity) return RS_ERR_INVALID_ARG;
@@ -1067,6 +1071,7 @@ rs_status rs_poly_encode(const rs_poly_plan *P, const void *const *data, void *c
 
 rs_status rs_poly_decode(const rs_poly_plan *P, void *const *blocks, size_t block_bytes, const int *erasures,
                          int n_erasures, void *stream) {
+  NvtxRange nvtx_("rs_poly_decode");
   rs_status rc = check_geometry(P, block_bytes);
   if (rc) return rc;
   if (!blocks || n_erasures < 0 || (n_erasures > 0 && !erasures)) return RS_ERR_INVALID_ARG;
@@ -1097,6 +1102,7 @@ rs_status rs_poly_decode(const rs_poly_plan *P, void *const *blocks, size_t bloc
 
 rs_status rs_poly_encode_batch(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
                                size_t block_stride, size_t block_bytes, void *stream) {
+  NvtxRange nvtx_("rs_poly_encode_batch");
   rs_status rc = check_strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
   if (rc) return rc;
   if (n_stripes == 0) return RS_OK;
@@ -1106,6 +1112,7 @@ rs_status rs_poly_encode_batch(const rs_poly_plan *P, void *stripes, size_t n_st
 
 rs_status rs_poly_decode_batch(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
                                size_t block_stride, size_t block_bytes, const int32_t *erasures, void *stream) {
+  NvtxRange nvtx_("rs_poly_decode_batch");
   rs_status rc = check_strided(P, stripes, n_stripes, stripe_stride, block_stride, block_bytes);
   if (rc) return rc;
   if (n_stripes == 0) return RS_OK;

@@ -19,6 +19,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only; a no-op unless a profiler (nsys, ncu) is attached
+
 #include "../../include/rs_poly.h"
 #include "gf.hpp"
 #include "jit.hpp"
@@ -255,6 +257,15 @@ struct DevBlob {
     p = nullptr;
     return e;
   }
+};
+
+// NVTX range around a C ABI call (SURVEY section 5 tracing): names the library's work in
+// profiler timelines.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
 };
 
 // ---- shared helpers (plan.cpp unless noted) ---------------------------------------
