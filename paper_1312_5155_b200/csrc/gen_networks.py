@@ -48,6 +48,10 @@ INSTANCES = [
 # Horner (~715 LOP3) + Q (~620 XORs) streams one block at a time.
 HORNER_W = (16,)
 
+# CSE flavour: cse3 factors pairs and triples by estimated 3-input-gate (LOP3) savings;
+# paar is the classic pair-only greedy (fewest 2-input XORs).
+CSE_MODE = os.environ.get("RS_GEN_CSE", "cse3")
+
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "rs_networks.cuh")
 
 
@@ -130,6 +134,53 @@ def paar(R: np.ndarray):
     return temps, rows
 
 
+def cse3(R: np.ndarray):
+    """Greedy CSE for 3-input XOR gates (one LOP3 each).  A row of r terms costs about
+    (r - 1) / 2 gates, so factoring a set of s variables shared by c rows saves about
+    (s - 1) c / 2 - 1 gates; repeatedly factor the pair or triple with the largest saving.
+    Returns (temps, rows): temps[t] = tuple of 2 or 3 vars XORed into var (nin + t);
+    rows[r] = sorted vars whose XOR is output r.  Rows <= 64 (column masks are uint64)."""
+    nrow, nin = R.shape
+    assert nrow <= 64
+    cols = [int(sum(1 << r for r in range(nrow) if R[r, c])) for c in range(nin)]
+    temps = []
+    while True:
+        arr = np.array(cols, dtype=np.uint64)
+        pc = np.bitwise_count(arr)
+        best, pick = 0.0, None
+        nv = len(cols)
+        for a in range(nv):
+            if pc[a] < 2:
+                continue
+            ab = arr[a] & arr[a + 1:]
+            cab = np.bitwise_count(ab)
+            for off in np.nonzero(cab >= 2)[0]:
+                b = a + 1 + int(off)
+                c2 = int(cab[off])
+                if c2 / 2 - 1 > best:
+                    best, pick = c2 / 2 - 1, (a, b)
+                if b + 1 < nv and c2 - 1 > best:  # else no triple within (a, b) can beat it
+                    c3 = np.bitwise_count(ab[off] & arr[b + 1:])
+                    j = int(np.argmax(c3))
+                    if c3[j] >= 2 and c3[j] - 1 > best:
+                        best, pick = float(c3[j] - 1), (a, b, b + 1 + j)
+        if pick is None:
+            break
+        common = cols[pick[0]]
+        for v in pick[1:]:
+            common &= cols[v]
+        for v in pick:
+            cols[v] &= ~common
+        cols.append(common)
+        temps.append(pick)
+    rows = [sorted(v for v in range(len(cols)) if (cols[v] >> r) & 1) for r in range(nrow)]
+    return temps, rows
+
+
+def CSE(R: np.ndarray):
+    return cse3(R) if CSE_MODE == "cse3" else paar(R)
+
+
 def gf_pow(a: int, e: int, w: int, poly: int) -> int:
     r = 1
     for _ in range(e):
@@ -178,13 +229,13 @@ def gf_bit_matrix(M: list[list[int]], w: int, poly: int) -> np.ndarray:
 
 def emit_horner(k: int, m: int, w: int, poly: int) -> str:
     R = gf_bit_matrix(horner_q(k, m, w, poly), w, poly)
-    temps, rows = paar(R)
+    temps, rows = CSE(R)
     nin = m * w
 
     def name(v: int) -> str:
         return f"h[{v}]" if v < nin else f"t{v - nin}"
 
-    xors = len(temps) + sum(max(0, len(r) - 1) for r in rows)
+    xors = sum(len(t) - 1 for t in temps) + sum(max(0, len(r) - 1) for r in rows)
     out = [
         f"// RS({k},{m}) over GF(2^{w}) / 0x{poly:X}: syndrome-form encoder.  Q = Vp^-1 diag(alpha^jm),",
         f"// bit-matrix {m * w}x{m * w} with {int(R.sum())} ones -> {xors} two-input XORs after CSE.",
@@ -193,8 +244,8 @@ def emit_horner(k: int, m: int, w: int, poly: int) -> str:
         f"  static constexpr int kXors = {xors};",
         f"  static __device__ __forceinline__ void run(const uint32_t (&h)[{nin}], uint32_t (&y)[{m * w}]) {{",
     ]
-    for t, (a, b) in enumerate(temps):
-        out.append(f"    const uint32_t t{t} = {name(a)} ^ {name(b)};")
+    for t, ops in enumerate(temps):
+        out.append(f"    const uint32_t t{t} = " + " ^ ".join(name(v) for v in ops) + ";")
     for r, terms in enumerate(rows):
         expr = " ^ ".join(name(v) for v in terms) if terms else "0u"
         out.append(f"    y[{r}] = {expr};")
@@ -213,12 +264,13 @@ def emit_instance(k: int, m: int, w: int, poly: int, gsize: int) -> str:
         j0, j1 = g * gsize, min(k, (g + 1) * gsize)
         sub = R[:, j0 * w: j1 * w]
         nin = (j1 - j0) * w
-        temps, rows = paar(sub)
+        temps, rows = CSE(sub)
 
         def name(v: int) -> str:
             return f"x[{v}]" if v < nin else f"t{v - nin}"
 
-        xors = len(temps) + sum(max(0, len(r) - 1) for r in rows) + (0 if g == 0 else sum(1 for r in rows if r))
+        xors = sum(len(t) - 1 for t in temps) + sum(max(0, len(r) - 1) for r in rows) + \
+            (0 if g == 0 else sum(1 for r in rows if r))
         total_xors += xors
         body += [
             f"// group {g}: data blocks {j0}..{j1 - 1}, {int(sub.sum())} ones, {len(temps)} temps, {xors} XORs",
@@ -226,8 +278,8 @@ def emit_instance(k: int, m: int, w: int, poly: int, gsize: int) -> str:
             f"  static constexpr int kFirstBlock = {j0}, kBlocks = {j1 - j0};",
             f"  static __device__ __forceinline__ void run(const uint32_t (&x)[{nin}], uint32_t (&y)[{m * w}]) {{",
         ]
-        for t, (a, b) in enumerate(temps):
-            body.append(f"    const uint32_t t{t} = {name(a)} ^ {name(b)};")
+        for t, ops in enumerate(temps):
+            body.append(f"    const uint32_t t{t} = " + " ^ ".join(name(v) for v in ops) + ";")
         for r, terms in enumerate(rows):
             expr = " ^ ".join(name(v) for v in terms) if terms else "0u"
             body.append(f"    y[{r}] = {expr};" if g == 0 else (f"    y[{r}] ^= {expr};" if terms else ""))

@@ -126,7 +126,10 @@ def evaluate_horner(src, cw_cols):
             for b in range(W):
                 S[base + b] = sum(((syms[c] >> b) & 1) << c for c in range(C))
         elif mm := re.fullmatch(r"const uint32_t (t\d+) = (.*);", line):
-            env[mm.group(1)] = val(mm.group(2).split("^")[0]) ^ val(mm.group(2).split("^")[1])
+            v = 0
+            for tok in mm.group(2).split("^"):
+                v ^= val(tok)
+            env[mm.group(1)] = v
         elif mm := re.fullmatch(r"y\[(\d+)\] = (.*);", line):
             v = 0
             for tok in mm.group(2).split("^"):
