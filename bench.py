@@ -359,9 +359,11 @@ def run_ours(args):
                      "kernel": f"{dom_name}; {moved} algorithmic bytes per call = S*(k+m)*B, avg {dom_ms:.4f} ms",
                      "peak_source": peak_src},
         "encode": {"gbs_user": round(user_bytes / (enc_avg / 1e3) / 1e9, 2), "ms": round(enc_avg, 4),
-                   "hbm_frac": round(moved / (enc_avg / 1e3) / 1e9 / peak, 4)},
+                   "hbm_frac": round(moved / (enc_avg / 1e3) / 1e9 / peak, 4),
+                   "ms_min_med_max": [round(min(enc_ms), 4), round(statistics.median(enc_ms), 4), round(max(enc_ms), 4)]},
         "decode": {"gbs_user": round(user_bytes / (dec_avg / 1e3) / 1e9, 2), "ms": round(dec_avg, 4),
-                   "hbm_frac": round(moved / (dec_avg / 1e3) / 1e9 / peak, 4)},
+                   "hbm_frac": round(moved / (dec_avg / 1e3) / 1e9 / peak, 4),
+                   "ms_min_med_max": [round(min(dec_ms), 4), round(statistics.median(dec_ms), 4), round(max(dec_ms), 4)]},
         "verified": {"mismatches": mismatches,
                      "how": "encode vs CPU oracle on sampled columns of 3 stripes (before and after timing); "
                             "decode restores all S*n*B bytes (exact device compare)"},
