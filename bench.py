@@ -189,6 +189,18 @@ def run_reference(args):
 # --------------------------------------------------------------------------------------
 # clocks during the timed region (NVML)
 # --------------------------------------------------------------------------------------
+def nvml_handle(pynvml, cuda_index: int):
+    """NVML handle of CUDA device `cuda_index`, matched by PCI address (NVML enumerates in its own
+    order and ignores CUDA_VISIBLE_DEVICES); NVML index `cuda_index` if that fails."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(cuda_index)
+        bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        return pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+    except Exception:
+        return pynvml.nvmlDeviceGetHandleByIndex(cuda_index)
+
+
 class ClockSampler:
     REASONS = {
         "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
@@ -208,7 +220,7 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._h = nvml_handle(pynvml, self.index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
             self.ok = True
         except Exception:
@@ -405,7 +417,7 @@ def gpu_local_cpus(index: int):
     try:
         import pynvml
         pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        h = nvml_handle(pynvml, index)
         words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
         cpus = {64 * i + b for i, mk in enumerate(words) for b in range(64) if (mk >> b) & 1}
         cpus &= os.sched_getaffinity(0)
