@@ -1,5 +1,6 @@
 """Seeded fuzz: random codes, geometries, alignments, erasure patterns, JIT modes and read
-policies -- encode, decode and diff-update against the oracle, bit for bit."""
+policies -- encode, verify (clean and one flipped bit), decode and diff-update against the
+oracle, bit for bit."""
 import numpy as np
 import pytest
 
@@ -40,6 +41,16 @@ def test_fuzz_against_oracle(case):
     plan.encode_batch(d)
     torch.cuda.synchronize()
     assert np.array_equal(d.cpu().numpy(), ref), "encode"
+    flags = torch.full((S,), 9, dtype=torch.int32, device="cuda")
+    plan.verify_batch(d, flags)
+    torch.cuda.synchronize()
+    assert flags.cpu().tolist() == [0] * S, "verify (clean)"
+    s_bad, b_bad, x_bad = int(rng.integers(S)), int(rng.integers(k + m)), int(rng.integers(B))
+    d[s_bad, b_bad, x_bad] ^= 0x20
+    plan.verify_batch(d, flags)
+    torch.cuda.synchronize()
+    assert [i for i, f in enumerate(flags.cpu().tolist()) if f] == [s_bad], "verify (one flip)"
+    d[s_bad, b_bad, x_bad] ^= 0x20
     er = np.full((S, m), -1, dtype=np.int32)
     for s in range(S):
         t = int(rng.integers(0, m + 1))
