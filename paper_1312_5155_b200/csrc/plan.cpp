@@ -151,6 +151,16 @@ rsb::jit::Spec jit_spec(const rs_poly_plan &P, const std::vector<int> &in, const
   return s;
 }
 
+// __launch_bounds__ min CTAs/SM of the w16 JIT kernels (RS_POLY_JIT_W16_MINB, default 3:
+// 168 registers, no spill; 4 caps them at 128 and spills ~400 B).
+int jit_w16_min_blocks() {
+  static const int v = [] {
+    const char *e = std::getenv("RS_POLY_JIT_W16_MINB");
+    return e ? (int)std::max(1L, std::min(std::strtol(e, nullptr, 10), 8L)) : 3;
+  }();
+  return v;
+}
+
 // Unroll factor of the Horner position loop in w16 JIT kernels (RS_POLY_JIT_UNROLL, 0 =
 // fully unrolled straight-line code).
 int jit_w16_unroll() {
@@ -174,7 +184,7 @@ rsb::jit::Spec encoder_spec(const rs_poly_plan &P) {
     s.T = P.m;
     s.M = rsb::horner_q(P.F, P.m);
     for (int j = P.k - 1; j >= 0; --j) s.seq.push_back(j);  // positions m+k-1 .. m
-    s.min_blocks = 3;
+    s.min_blocks = jit_w16_min_blocks();
     s.loop_unroll = jit_w16_unroll();
     s.pos_top = P.m + P.k - 1;
     s.k = P.k;
@@ -198,7 +208,7 @@ rsb::jit::Spec decoder_spec(const rs_poly_plan &P, const PatternHost &ph) {
       const int b = pos >= P.m ? pos - P.m : P.k + pos;  // inverse of rsb::position
       s.seq.push_back(er[b] ? -1 : b);
     }
-    s.min_blocks = 3;
+    s.min_blocks = jit_w16_min_blocks();
     s.loop_unroll = jit_w16_unroll();
     s.pos_top = P.n - 1;
     s.k = P.k;
@@ -770,7 +780,7 @@ rsb::jit::Spec verify_spec(const rs_poly_plan &P) {
     s.poly = P.poly;
     s.T = m;
     for (int pos = n - 1; pos >= 0; --pos) s.seq.push_back(pos >= m ? pos - m : P.k + pos);
-    s.min_blocks = 3;
+    s.min_blocks = jit_w16_min_blocks();
   } else {
     s.group_blocks = 10;  // n * 8 input planes in CSE groups of 10 blocks
   }
