@@ -270,3 +270,32 @@ def test_jit_pointer_api(k, m, w, poly):
     for b in range(k + m):
         assert np.array_equal(blocks[b].cpu().numpy(), ref[b]), b
     assert plan.stats()["jit_launches"] >= 1
+
+
+def test_no_device_memory_growth_over_many_calls():
+    """400 encode/decode/update/verify calls: the per-call blobs, pinned slots and staging are
+    reused or freed (device free memory stays put once the JIT modules are loaded)."""
+    k, m, B, S = 10, 4, 32 * 1024, 24
+    m_ = rs()
+    plan = m_.Plan(k, m)
+    ref = encoded(k, m, 8, P8, B, S, seed=99)
+    d = torch.from_numpy(ref).cuda()
+    er = synth.erasure_table("C5", 4, S)
+    plan.prepare(er)
+    flags = torch.zeros(S, dtype=torch.int32, device="cuda")
+    old = d[:, [3]].clone()
+
+    def burst(n):
+        for _ in range(n):
+            plan.encode_batch(d)
+            plan.decode_batch(d, er)
+            plan.update_batch(d, [3], old)
+            plan.verify_batch(d, flags)
+        torch.cuda.synchronize()
+
+    burst(20)
+    free0 = torch.cuda.mem_get_info()[0]
+    burst(100)
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < (64 << 20), (free0, free1)
+    assert torch.equal(d.cpu(), torch.from_numpy(ref))
