@@ -146,3 +146,18 @@ def test_placement_p2p_on_gpu(world, k, m):
     for r in range(world):
         for (s, b), t in stores[r].items():
             assert np.array_equal(t.cpu().numpy(), ref[s, b]), (r, s, b)
+
+
+def test_symmetric_memory_path_one_rank():
+    """encode_distributed_p2p over torch symmetric memory (one-rank NCCL group, in a
+    subprocess so the process group does not leak into other tests)."""
+    import os
+    import random
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SYMM_PORT=str(random.randint(30000, 39000)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "symm_smoke.py")], capture_output=True,
+                         text=True, timeout=300, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "bad 0" in out.stdout, out.stdout
