@@ -78,3 +78,21 @@ def test_reference_arm_under_torchrun_prints_once():
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert np.isfinite(d["ms_per_step"])
+
+
+def test_bench_verification_catches_one_flipped_byte():
+    """T6 negative test of the harness: bench.py's oracle check of sampled columns reports a
+    single corrupted parity byte (CPU tensors; the check itself is host-side)."""
+    import torch
+    sys.path.insert(0, ROOT)
+    import bench
+    import oracle
+    import synth
+    c = bench.workload("C1", 0)
+    c["stripes"] = 3
+    st = synth.stripes_array(c["seed"], range(3), c["k"], c["m"], c["block_bytes"])
+    oracle.encode_bulk(st, c["k"], c["m"], c["w"], c["poly"], threads=2)
+    t = torch.from_numpy(st)
+    assert bench.verify_encode_sampled(t, c) == 0
+    t[1, c["k"] + 2, 17] ^= 0x01            # inside the sampled first 32 KiB of stripe S/2
+    assert bench.verify_encode_sampled(t, c) == 1
