@@ -2,10 +2,12 @@
 //
 // For a fixed GF matrix M (outputs x inputs) -- an erasure pattern's decode
 // matrix R_E = V_E^{-1} A_E (P:244-303 with Opt1/Opt3 of P:319-323 taken to
-// code generation), or the parity map of a code without a compiled network --
+// code generation), the parity map of a code without a compiled network, a
+// diff-update / partial-encode / XOR "linear job", or the syndrome map of verify --
 // this builds the GF(2) bit-matrix, reduces it with the same greedy CSE as
-// gen_networks.py and compiles a straight-line kernel: every HBM byte of the
-// n-t survivors read once, the t outputs written once, no runtime tables.
+// gen_networks.py (pairs and triples, for 3-input LOP3 gates) and compiles a
+// straight-line kernel: every HBM byte of the inputs read once, the outputs written
+// once, no runtime tables.  w16 decoders/encoders use the syndrome (Horner) form.
 #pragma once
 #include <cstdint>
 #include <string>

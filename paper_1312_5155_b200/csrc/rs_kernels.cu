@@ -6,17 +6,22 @@
 //   decode: the erased symbols of each column from the survivors (two-step
 //           decode).
 //
-// Two kernel families:
+// Compiled kernel families (the per-pattern decoders are generated at
+// run time by jit.cpp):
 //   * sliced_kernel<K,M,W,POLY,DECODE>: each thread owns 32 columns; it loads
 //     32*W/8 bytes of each block with 256-bit loads, transposes them into W
-//     bit-planes (three/four delta swaps), applies the compile-time GF(2)
-//     network RsNet (parity map of g, P:459 + bit-matrix form) and
-//     transposes back.  Decode re-encodes the surviving data (erased data
-//     zeroed), XORs the received parity to get Delta = H_par^{-1}-side
-//     residue, and solves the t erased symbols with the runtime t x m matrix
-//     W = V_E^{-1} H_par[0:t,:] through split-nibble tables in shared memory.
-//   * generic_kernel<W>: out_r = sum_s M[r][s] in_s with runtime split-nibble
-//     tables (any k, m, any erasure pattern, any alignment, ragged tails).
+//     bit-planes (three/four delta swaps) and transposes the results back.
+//     w8 encode: the compile-time GF(2) network RsNet (parity map of g, in
+//     bit-matrix form; CSE for 3-input gates).  w16 encode: the syndrome
+//     form -- Horner over the data blocks with step alpha^j, then the
+//     network RsQNet = Vp^{-1} diag(alpha^{jm}) (the decoder used to encode).
+//     DECODE (the table fallback): re-encode the surviving data (erased data
+//     zeroed), XOR the received parity to get Delta, and solve the t erased
+//     symbols with the runtime t x m matrix W = V_E^{-1} H_par[0:t,:] through
+//     split-nibble tables in shared memory.
+//   * generic_kernel<W, VERIFY>: out_r = sum_s M[r][s] in_s with runtime split-nibble
+//     tables (any k, m, any erasure pattern, any alignment, ragged tails); VERIFY
+//     ORs the outputs (syndromes) into a per-stripe flag instead of storing them.
 // Every HBM byte of a stripe is read once or written once: (k+m)*B per pass.
 #include <atomic>
 #include <cstdio>
