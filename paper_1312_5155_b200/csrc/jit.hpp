@@ -35,11 +35,6 @@ struct Spec {
   uint32_t poly = 0;
   std::vector<int> seq;
   int T = 0;
-  // loop_unroll > 0: positions after the first survivor in a loop unrolled that many times
-  // (seq[i] at position pos_top - i; block of a position: data pos - m, parity k + pos);
-  // 0: straight-line code with the erased set compiled in
-  int loop_unroll = 0;
-  int pos_top = 0, k = 0, m = 0;
   // verify: compute the outputs (syndromes) but, instead of storing them, flag the stripe
   // (Args::flags[s] |= 1) when any is non-zero
   bool verify = false;

@@ -161,16 +161,6 @@ int jit_w16_min_blocks() {
   return v;
 }
 
-// Unroll factor of the Horner position loop in w16 JIT kernels (RS_POLY_JIT_UNROLL, 0 =
-// fully unrolled straight-line code).
-int jit_w16_unroll() {
-  static const int v = [] {
-    const char *e = std::getenv("RS_POLY_JIT_UNROLL");
-    return e ? (int)std::max(0L, std::min(std::strtol(e, nullptr, 10), 16L)) : 0;
-  }();
-  return v;
-}
-
 // The encoder kernel of a code without a compiled network: w = 8 the parity-map
 // network, w = 16 the syndrome form (Horner over the data, then Q).
 rsb::jit::Spec encoder_spec(const rs_poly_plan &P) {
@@ -185,10 +175,6 @@ rsb::jit::Spec encoder_spec(const rs_poly_plan &P) {
     s.M = rsb::horner_q(P.F, P.m);
     for (int j = P.k - 1; j >= 0; --j) s.seq.push_back(j);  // positions m+k-1 .. m
     s.min_blocks = jit_w16_min_blocks();
-    s.loop_unroll = jit_w16_unroll();
-    s.pos_top = P.m + P.k - 1;
-    s.k = P.k;
-    s.m = P.m;
   }
   return s;
 }
@@ -209,10 +195,6 @@ rsb::jit::Spec decoder_spec(const rs_poly_plan &P, const PatternHost &ph) {
       s.seq.push_back(er[b] ? -1 : b);
     }
     s.min_blocks = jit_w16_min_blocks();
-    s.loop_unroll = jit_w16_unroll();
-    s.pos_top = P.n - 1;
-    s.k = P.k;
-    s.m = P.m;
   }
   return s;
 }

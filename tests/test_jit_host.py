@@ -64,42 +64,7 @@ def evaluate_horner(src, cw_cols):
         mm = re.fullmatch(r"S\[(\d+)\]", tok)
         return S[int(mm.group(1))] if mm else env[tok]
 
-    lines = [ln.strip() for ln in body.splitlines()]
-    # compact form: "#pragma unroll N" + "for (int i = A; i < B; ++i) { if ((MASK >> i) & 1) {erased}
-    # else {survivor} }" is expanded into straight-line statements, block index substituted
-    out_lines, i = [], 0
-    while i < len(lines):
-        mm = re.fullmatch(r"for \(int i = (\d+); i < (\d+); \+\+i\) \{", lines[i])
-        if not mm:
-            if not lines[i].startswith("#pragma unroll"):
-                out_lines.append(lines[i])
-            i += 1
-            continue
-        lo, hi = int(mm.group(1)), int(mm.group(2))
-        emask = int(re.fullmatch(r"if \(\((\d+)ull >> i\) & 1ull\) \{", lines[i + 1]).group(1))
-        j = i + 2
-        er_body = []
-        while lines[j] != "} else {":
-            er_body.append(lines[j])
-            j += 1
-        j += 1
-        sv_body = []
-        while lines[j] != "}":
-            sv_body.append(lines[j])
-            j += 1
-        assert lines[j + 1] == "}"
-        pos_top = int(re.fullmatch(r"const int pos = (\d+) - i;", sv_body[0]).group(1))
-        mb = re.fullmatch(r"const int b = pos >= (\d+) \? pos - (\d+) : (\d+) \+ pos;", sv_body[1])
-        M_, K_ = int(mb.group(1)), int(mb.group(3))
-        for it in range(lo, hi):
-            if (emask >> it) & 1:
-                out_lines += er_body
-            else:
-                pos = pos_top - it
-                blk = pos - M_ if pos >= M_ else K_ + pos
-                for ln in sv_body[2:]:
-                    out_lines.append(ln.replace("blkp(a, s, b)", f"blkp(a, s, {blk})"))
-        i = j + 2
+    out_lines = [ln.strip() for ln in body.splitlines()]
     for line in out_lines:
         if mm := re.fullmatch(r"load_unit<\d+>\(blkp\(a, s, (\d+)\) \+ off, x\);", line):
             x = dict(enumerate(planes(int(mm.group(1)))))
