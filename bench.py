@@ -68,6 +68,25 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def copy_peak_in_run(dev) -> float:
+    """GB/s of b.copy_(a) on 1 Gi bf16 elements (read + write bytes, best of 10, CUDA events):
+    the MEASURED_PEAKS.json method, repeated in this run on this box."""
+    import torch
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+    b = torch.empty_like(a)
+    best = float("inf")
+    for _ in range(11):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * (1 << 30) * 2 / (best / 1e3) / 1e9
+
+
 def ncu_traffic(cfg: str, op: str):
     """DRAM bytes per call of the dominant kernel from the committed ncu capture (or None)."""
     try:
@@ -351,6 +370,7 @@ def run_ours(args):
     moved = S * (k + m) * B                     # HBM bytes per pass (read once or written once)
     value = step_throughput(user_bytes, 2, world, total_ms / K)
     peak, peak_src = hbm_peak()
+    peak_run = copy_peak_in_run(dev)
     jst = plan.stats()
     dec_kernel = "rs_jit (per-pattern NVRTC XOR network)" if jst["jit_launches"] else "sliced_kernel decode (tables)"
     dom_ms, dom_name = (dec_avg, "decode: " + dec_kernel) if dec_avg >= enc_avg else (enc_avg, "encode: sliced_kernel")
@@ -378,7 +398,9 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": f"{dom_name}; {moved} algorithmic bytes per call = S*(k+m)*B, avg {dom_ms:.4f} ms",
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     "peak_in_run": round(peak_run, 1), "frac_in_run": round(achieved / peak_run, 4),
+                     "frac_nominal_8tbs": round(achieved / 8000.0, 4)},
         "encode": {"gbs_user": round(user_bytes / (enc_avg / 1e3) / 1e9, 2), "ms": round(enc_avg, 4),
                    "hbm_frac": round(moved / (enc_avg / 1e3) / 1e9 / peak, 4),
                    "ms_min_med_max": [round(min(enc_ms), 4), round(statistics.median(enc_ms), 4), round(max(enc_ms), 4)]},
