@@ -344,10 +344,44 @@ def run_configs(a):
     bad += 0 if torch.equal(st, golden) else 1
     enc = timed(lambda: plan.encode_batch(st), 200, 20, stream)
     dec = timed(lambda: plan.decode_batch(st, er), 200, 20, stream)
+    # launch-bound: the same encode + decode captured once into a CUDA graph and replayed
+    # (both calls are single launches with arguments by value on this path: nothing to upload)
+    graph_us = None
+    try:
+        cap = torch.cuda.Stream()
+        with torch.cuda.stream(cap):
+            plan.encode_batch(st, stream=cap)
+            plan.decode_batch(st, er, stream=cap)
+        torch.cuda.synchronize()
+        g_enc, g_dec = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_enc, stream=cap):
+            plan.encode_batch(st, stream=cap)
+        with torch.cuda.graph(g_dec, stream=cap):
+            plan.decode_batch(st, er, stream=cap)
+        for _ in range(20):
+            g_enc.replay()
+            g_dec.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(200):
+            g_enc.replay()
+            g_dec.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        graph_us = round(e0.elapsed_time(e1) / 200 * 1e3, 1)
+        golden2 = st.clone()
+        st[0, torch.from_numpy(er[0].astype(np.int64)).cuda()] = 0
+        g_dec.replay()                                   # the captured decode restores them
+        torch.cuda.synchronize()
+        bad += 0 if torch.equal(st, golden2) else 1
+    except Exception as ex:  # noqa: BLE001
+        graph_us = f"capture failed: {ex}"[:200]
     print(json.dumps({"config": "C1", "workload": "RS(10,4) GF(2^8), 1 stripe x 10 x 64 KiB, 4 erasures",
                       "encode_us": {"median": round(statistics.median(enc) * 1e3, 1), "min": round(min(enc) * 1e3, 1)},
                       "decode_us": {"median": round(statistics.median(dec) * 1e3, 1), "min": round(min(dec) * 1e3, 1)},
                       "erasures": er[0].tolist(), "verified": bad == 0,
+                      "cuda_graph_encode_plus_decode_us": graph_us,
                       "note": "896 KiB per pass: launch-latency bound (encode: one kernel; decode: one JIT kernel, nothing uploaded); includes the Python binding per call"}),
           flush=True)
     # C2: RS(6,3) 256 x 1 MiB encode; decode sweep on stripes 0..3 (9 singles + 20 data triples each)
