@@ -32,6 +32,14 @@
  * Errors are returned synchronously after argument validation and before any
  * device work; on a validation error nothing is written.  Launch failures
  * return RS_ERR_CUDA; asynchronous device faults surface at stream sync.
+ *
+ * CUDA graph capture: a call that launches kernels only (arguments by value, plan-
+ * owned device constants) may be captured on the caller's stream once the plan has
+ * run once on that device: rs_poly_encode_batch, rs_poly_verify_batch, and
+ * rs_poly_decode_batch when every pattern of the batch has its JIT kernel (after
+ * rs_poly_prepare), the blocks have no ragged tail and each pattern's stripes are
+ * contiguous (e.g. one stripe, one shared pattern, or all patterns distinct).  Calls that upload per-call
+ * constants return RS_ERR_CUDA when the stream is capturing (nothing is enqueued).
  * There is no CPU fallback: every entry point that computes runs CUDA kernels.
  */
 #ifndef RS_POLY_H

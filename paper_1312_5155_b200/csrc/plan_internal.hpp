@@ -248,6 +248,11 @@ struct DevBlob {
   cudaStream_t st = nullptr;
   cudaError_t upload(const rs_poly_plan &P, const Blob &b, cudaStream_t s) {
     st = s;
+    // The blob is copied from a pinned slot that later calls reuse: a CUDA graph replaying
+    // this copy would read another call's constants.  Refuse to be captured.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+      return cudaErrorStreamCaptureUnsupported;
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p), std::max<size_t>(b.h.size(), 16), s);
     if (e != cudaSuccess) return e;
     return upload_pinned(P, p, b.h.data(), b.h.size(), s);

@@ -299,3 +299,42 @@ def test_no_device_memory_growth_over_many_calls():
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 < (64 << 20), (free0, free1)
     assert torch.equal(d.cpu(), torch.from_numpy(ref))
+
+
+def test_cuda_graph_capture():
+    """Calls that only launch kernels can be captured in a CUDA graph (replays are bit-exact);
+    a call that would upload per-call constants refuses capture (RS_ERR_CUDA) instead of
+    baking a reused host buffer into the graph."""
+    k, m, B, S = 10, 4, 64 * 1024, 4
+    m_ = rs()
+    plan = m_.Plan(k, m)
+    ref = encoded(k, m, 8, P8, B, S, seed=111)
+    d = torch.from_numpy(ref).cuda()
+    er_same = np.tile(np.array([[1, 4, 10, 13]], dtype=np.int32), (S, 1))   # one shared pattern
+    plan.prepare(er_same)
+    cap = torch.cuda.Stream()
+    with torch.cuda.stream(cap):                      # run once on the device before capturing
+        plan.encode_batch(d, stream=cap)
+        plan.decode_batch(d, er_same, stream=cap)
+    torch.cuda.synchronize()
+    g_enc, g_dec = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_enc, stream=cap):
+        plan.encode_batch(d, stream=cap)
+    with torch.cuda.graph(g_dec, stream=cap):
+        plan.decode_batch(d, er_same, stream=cap)
+    d[:, k:] = 0
+    g_enc.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    d[:, [1, 4, 10, 13]] = 0x77
+    g_dec.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    # patterns A, B, A, B: A's stripes are not contiguous -> per-call stripe lists to upload
+    er_mixed = np.array([[1, 4, 10, 13], [0, 2, 3, 5], [1, 4, 10, 13], [0, 2, 3, 5]], dtype=np.int32)
+    plan.prepare(er_mixed)
+    g_bad = torch.cuda.CUDAGraph()
+    with pytest.raises((m_.RSError, RuntimeError)):
+        with torch.cuda.graph(g_bad, stream=cap):
+            plan.decode_batch(d, er_mixed, stream=cap)
+    torch.cuda.synchronize()
