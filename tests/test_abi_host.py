@@ -11,7 +11,9 @@ import ctypes
 import glob
 import os
 import re
+import subprocess
 import sys
+import tempfile
 
 import numpy as np
 import pytest
@@ -244,3 +246,24 @@ def test_generated_header_is_current():
     import gen_networks
     head = open(os.path.join(PKG, "csrc", "rs_networks.cuh")).read(4096)
     assert f"generator-digest: {gen_networks.source_digest()}" in head
+
+
+def test_headers_are_plain_c_and_demo_links():
+    """include/*.h compile as C99 (no C++ in the ABI), and the C demo links against the
+    built libraries (tools/c_api_demo.c; it runs on the GPU in tests/test_gpu_c_api.py)."""
+    import shutil
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(PKG)
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "h.c")
+        open(src, "w").write('#include "rs_poly.h"\n#include "rs_synth.h"\nint main(void){return 0;}\n')
+        r = subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-pedantic", "-fsyntax-only", "-I",
+                            os.path.join(root, "include"), src], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        r = subprocess.run([gcc, "-std=c99", "-O2", "-I", os.path.join(root, "include"), "-I",
+                            "/usr/local/cuda/include", os.path.join(root, "tools", "c_api_demo.c"), "-L", PKG,
+                            "-lrs_poly", "-lrs_synth", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                            "-o", os.path.join(d, "demo")], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
