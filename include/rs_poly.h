@@ -165,6 +165,11 @@ rs_status rs_poly_update(const rs_poly_plan *plan, const int *data_idx, int n_ch
                          const void *const *old_data, const void *const *new_data,
                          void *const *parity, size_t block_bytes, void *stream);
 
+/* Compile (NVRTC) and cache the diff-update kernel of the changed set data_idx[0..c-1],
+ * blocking until it is ready, so that the first rs_poly_update* call for that set does not
+ * run on the table kernel while it compiles.  Host + NVRTC only; no kernel runs. */
+rs_status rs_poly_prepare_update(const rs_poly_plan *plan, const int *data_idx, int n_changed);
+
 /* Batched diff-update: `stripes` ([S][n][B] as in rs_poly_encode_batch) holds the NEW
  * data (already in place) and the OLD parity, which is updated in place; the old
  * contents of the changed blocks are in `old_blocks` at old_blocks + s*old_stripe_stride

@@ -257,6 +257,17 @@ rs_status rs_poly_xor_reduce(const rs_poly_plan *P, void *const *dst, const void
   return linear_impl(P, *lh, ptrs, n_stripes, bytes, static_cast<cudaStream_t>(stream));
 }
 
+rs_status rs_poly_prepare_update(const rs_poly_plan *P, const int *data_idx, int n_changed) {
+  if (!P) return RS_ERR_INVALID_ARG;
+  std::vector<int> idx, order;
+  rs_status rc = parse_update(P, data_idx, n_changed, idx, order);
+  if (rc) return rc;
+  if (n_changed == 0 || P->jit_mode == RS_JIT_OFF || !jit_eligible(*P, P->m)) return RS_OK;
+  auto uh = update_host(*P, idx);
+  jit_get(*P, JitKey{kJitLinear, MaskKey{(uint64_t)uh->id, 0, 0, 0}}, [&] { return linear_spec(*P, *uh); }, true);
+  return RS_OK;
+}
+
 size_t rs_poly_update_jit_source(const rs_poly_plan *P, const int *data_idx, int n_changed, char *buf,
                                  size_t cap) {
   if (!P || n_changed < 1 || !jit_eligible(*P, P->m)) return 0;

@@ -47,6 +47,7 @@ _lib.rs_poly_update.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]
 _lib.rs_poly_update_batch.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _i32, _vp, _sz, _sz, _vp]
 _lib.rs_poly_update_jit_source.argtypes = [_vp, _vp, _i32, ctypes.c_char_p, _sz]
 _lib.rs_poly_update_jit_source.restype = _sz
+_lib.rs_poly_prepare_update.argtypes = [_vp, _vp, _i32]
 _lib.rs_poly_ablation_decode.argtypes = [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _i32, _i32, _vp]
 _lib.rs_poly_encode_partial.argtypes = [_vp, _vp, _i32, _vp, _vp, _sz, _sz, _i32, _vp]
 _lib.rs_poly_xor_reduce.argtypes = [_vp, _vp, _vp, _i32, _sz, _sz, _vp]
@@ -250,6 +251,12 @@ class Plan:
         ost = old_blocks.stride() if hasattr(old_blocks, "stride") else old_blocks.strides
         _check(_lib.rs_poly_update_batch(self._h, ptr, S, ss, bs, B, ix, c, _ptr(old_blocks), ost[0], ost[1],
                                          _stream(stream)), "rs_poly_update_batch")
+
+    def prepare_update(self, data_idx) -> None:
+        """Compile the diff-update kernel for this changed set now (rs_poly_prepare_update)."""
+        idx = list(data_idx)
+        ix = (ctypes.c_int * max(1, len(idx)))(*idx)
+        _check(_lib.rs_poly_prepare_update(self._h, ix, len(idx)), "rs_poly_prepare_update")
 
     def update_jit_source(self, data_idx) -> str:
         idx = list(data_idx)

@@ -94,3 +94,24 @@ def test_update_errors_and_noop():
     n0 = m_.launch_count()
     plan.update_batch(dev, [], torch.zeros((2, 0, 4096), dtype=torch.uint8, device="cuda"))
     assert m_.launch_count() == n0
+
+
+def test_prepare_update_compiles_before_the_first_call():
+    k, m, B, S = 10, 4, 64 * 1024, 3
+    m_ = rs()
+    plan = m_.Plan(k, m)                       # background JIT mode
+    plan.prepare_update([2, 7])
+    st = plan.stats()
+    assert st["jit_ready"] >= 1 and st["jit_pending"] == 0
+    old = encoded(k, m, 8, P8, B, S, seed=33)
+    new = old.copy()
+    new[:, [2, 7]] ^= 0x5A
+    want = new.copy()
+    oracle.encode_bulk(want, k, m, 8, P8, threads=4)
+    d = torch.from_numpy(new).cuda()
+    d[:, k:] = torch.from_numpy(old[:, k:]).cuda()
+    n0 = plan.stats()["jit_launches"]
+    plan.update_batch(d, [7, 2], torch.from_numpy(np.ascontiguousarray(old[:, [7, 2]])).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), want)
+    assert plan.stats()["jit_launches"] == n0 + 1      # the first call already used the JIT kernel
