@@ -190,10 +190,17 @@ def run_sweep(a):
     # Fig. 4: m sweep at k = 10 (m = 5, 6 use the JIT encoder)
     for m in (2, 3, 5, 6):
         pts.append(dict(k=10, m=m, B=4 * MiB, t=m, policy=0, fig="Fig4 m"))
+    # GF(2^16) (C4's code, not in the paper's figures): erasure count, both read policies
+    for t in (1, 2, 3, 4):
+        for pol in (0, 1):
+            pts.append(dict(k=12, m=4, B=4 * MiB, t=t, policy=pol, fig="w16 erasures", w=16, poly=0x1100B))
+    if a.figs:
+        pts = [p for p in pts if any(p["fig"].startswith(f) for f in a.figs.split(","))]
     bad = 0
     for p in pts:
         S = max(1, data_target // (p["k"] * p["B"]))
-        r = sweep_point(p["k"], p["m"], p["B"], S, p["t"], p["policy"], a.steps, a.warmup, p["fig"])
+        r = sweep_point(p["k"], p["m"], p["B"], S, p["t"], p["policy"], a.steps, a.warmup, p["fig"],
+                        w=p.get("w", 8), poly=p.get("poly", 0x11D))
         bad += r["verified"]["mismatches"]
         print(json.dumps(r), flush=True)
     return 0 if bad == 0 else 1
@@ -466,6 +473,7 @@ def main():
     ap.add_argument("what", choices=["update", "sweep", "ablation", "placement", "configs", "verify"])
     ap.add_argument("--world", type=int, default=8, help="placement: ranks of the emulated layout")
     ap.add_argument("--data-gib", type=int, default=20, help="sweep: user data per point")
+    ap.add_argument("--figs", default="", help="sweep: comma-separated figure-label prefixes to run")
     ap.add_argument("--config", default="C5")
     ap.add_argument("--changed", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
