@@ -384,6 +384,41 @@ cudaError_t launch_generic_range(const rs_poly_plan &P, const Geometry &G, uint6
 
 // Copy `bytes` at `src` to device `dst` on stream `s` through one of the plan's pinned
 // slots (reused once its previous copy has completed); pageable only if no slot can be had.
+// Process-wide pool (one per device) for the per-call blobs.  The default pool returns its
+// memory to the driver at every synchronize (release threshold 0), so a call after a
+// synchronize would re-map its blob: ~0.2 ms of host time before the first launch, with the
+// GPU idle.  This pool keeps up to 64 MiB.  It lives for the process (never destroyed:
+// destroying pools while other threads' plans tear down was measured to hang).
+cudaError_t blob_pool(cudaMemPool_t *out) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  e = cudaMemPoolCreate(&pool, &props);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = 64ull << 20;  // blobs are small (constants, stripe lists, pointer tables)
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  if (e != cudaSuccess) {
+    cudaMemPoolDestroy(pool);
+    return e;
+  }
+  pools[dev] = pool;
+  *out = pool;
+  return cudaSuccess;
+}
+
 cudaError_t upload_pinned(const rs_poly_plan &P, void *dst, const void *src, size_t bytes, cudaStream_t s) {
   // At most kMaxSlots pinned slots.  When all are in flight the host is at least that
   // many calls ahead of the GPU, so it waits for the oldest copy instead of allocating:
@@ -559,6 +594,28 @@ const rsb::jit::Kernel *pattern_jit(const rs_poly_plan &P, const PatternHost &ph
 // patterns are dealt round-robin over 1 + N chains forked from and joined back to `st`.
 // dev_lists: device base of the per-pattern stripe lists (grp_off), or nullptr when every
 // group is a contiguous stripe range (passed by value).
+// RS_POLY_HOST_PROFILE=1: per-call host time of each decode phase on stderr (diagnostics)
+struct HostProfile {
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  std::string line;
+  HostProfile() : on(enabled()), t(on ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{}) {}
+  static bool enabled() {
+    static const bool v = std::getenv("RS_POLY_HOST_PROFILE") != nullptr;
+    return v;
+  }
+  void mark(const char *what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    line += std::string(" ") + what + "=" +
+            std::to_string(std::chrono::duration<double, std::micro>(n - t).count()).substr(0, 8) + "us";
+    t = n;
+  }
+  ~HostProfile() {
+    if (on && !line.empty()) std::fprintf(stderr, "[rs_poly host]%s\n", line.c_str());
+  }
+};
+
 cudaError_t launch_jit_chains(const rs_poly_plan &P, const std::vector<const rsb::jit::Kernel *> &jk,
                               const std::vector<std::vector<int32_t>> &groups, const Geometry &G, uint64_t body,
                               const uint8_t *dev_lists, const std::vector<size_t> &grp_off, cudaStream_t st) {
@@ -609,7 +666,9 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   std::vector<std::shared_ptr<const PatternHost>> pats;
   std::vector<MaskKey> keys;
   std::vector<int32_t> idx;
+  HostProfile hp;
   rs_status rc = collect_patterns(P, rows, pats, keys, idx);
+  hp.mark("collect");
   if (rc) return rc;
   if (pats.empty()) return RS_OK;
   const uint64_t UB = 32ull * (uint64_t)P->w / 8;
@@ -622,6 +681,7 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
       jk[i] = pattern_jit(*P, *pats[i], keys[i], false);
       any_jit = any_jit || jk[i];
     }
+  hp.mark("jit_lookup");
   // the table-driven bit-sliced decode reads every survivor: not under RS_READ_K_SURVIVORS
   const bool sliced_rt = P->sliced && P->read_policy == RS_READ_ALL_SURVIVORS;
   if (!sliced_rt && !any_jit) body = 0;
@@ -643,8 +703,11 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   bool contig = true;
   for (const auto &gr : groups)
     for (size_t q = 1; q < gr.size() && contig; ++q) contig = gr[q] == gr[0] + (int32_t)q;
-  if (any_jit && !any_rt && !ptrs && contig && body * UB == G.block_bytes)
-    return cuda_status(launch_jit_chains(*P, jk, groups, G, body, nullptr, {}, st));
+  if (any_jit && !any_rt && !ptrs && contig && body * UB == G.block_bytes) {
+    const rs_status r = cuda_status(launch_jit_chains(*P, jk, groups, G, body, nullptr, {}, st));
+    hp.mark("launch(lean)");
+    return r;
+  }
   Blob b;
   size_t ptrs_off = SIZE_MAX;
   if (ptrs) ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);
@@ -682,8 +745,10 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   std::memcpy(b.h.data() + generic_pats_off, gps.data(), sizeof(rsb::GenericPat) * gps.size());
   const uint32_t smem = max_in * (P->w == 8 ? 128 : 512);
 
+  hp.mark("blob");
   DevBlob d;
   cudaError_t e = d.upload(*P, b, st);
+  hp.mark("upload");
   if (e == cudaSuccess && ptrs) G.L.ptrs = reinterpret_cast<const uint64_t *>(d.p + ptrs_off);
   // table-driven body for stripes without a ready JIT kernel
   if (e == cudaSuccess && body && any_rt) {
@@ -697,6 +762,7 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
     e = launch_generic_range(*P, G, body * UB, G.block_bytes, d.p, generic_pats_off, idx_off, tables_off,
                              max_groups, smem, st);
   if (e == cudaSuccess && any_jit) e = launch_jit_chains(*P, jk, groups, G, body, d.p, grp_off, st);
+  hp.mark("launch");
   cudaError_t ef = d.release();
   return cuda_status(e != cudaSuccess ? e : ef);
 }

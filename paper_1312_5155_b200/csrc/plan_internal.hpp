@@ -243,6 +243,8 @@ struct Geometry {
 
 cudaError_t upload_pinned(const rs_poly_plan &P, void *dst, const void *src, size_t bytes, cudaStream_t s);
 
+cudaError_t blob_pool(cudaMemPool_t *out);  // plan.cpp
+
 struct DevBlob {
   uint8_t *p = nullptr;
   cudaStream_t st = nullptr;
@@ -253,7 +255,10 @@ struct DevBlob {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
       return cudaErrorStreamCaptureUnsupported;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p), std::max<size_t>(b.h.size(), 16), s);
+    cudaMemPool_t pool = nullptr;
+    cudaError_t e = blob_pool(&pool);
+    if (e == cudaSuccess)
+      e = cudaMallocFromPoolAsync(reinterpret_cast<void **>(&p), std::max<size_t>(b.h.size(), 16), pool, s);
     if (e != cudaSuccess) return e;
     return upload_pinned(P, p, b.h.data(), b.h.size(), s);
   }
