@@ -324,7 +324,11 @@ cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32
   if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
   void *args[] = {&a};
   rsb::count_launch();
-  if (!pdl)
+  static const bool pdl_on = [] {  // RS_POLY_PDL=0 turns the chaining off (measurement knob)
+    const char *e = std::getenv("RS_POLY_PDL");
+    return !(e && e[0] == '0');
+  }();
+  if (!pdl || !pdl_on)
     return cudaLaunchKernel(reinterpret_cast<const void *>(k.fn), dim3((unsigned)grid), dim3(kSlicedThreads), args,
                             0, st);
   // programmatic dependent launch (the generated kernels trigger at entry and wait at exit)
