@@ -45,6 +45,7 @@ struct Kernel {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t fn = nullptr;
   int xors = 0;
+  int w = 8;            // symbol width of the spec it was generated from (grid sizing)
   bool cached = false;  // loaded from the on-disk cubin cache
   double compile_ms = 0;
   std::string log;

@@ -236,6 +236,7 @@ const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const JitKey &key, const 
       const std::string src = rsb::jit::source(*F, spec, &xors);
       auto k = std::make_shared<rsb::jit::Kernel>(rsb::jit::compile(src));
       k->xors = xors;
+      k->w = spec.w;
       if (!k->ok) {  // loud, once per process (the pattern then runs on the table kernel)
         static std::atomic<int> reported{0};
         if (reported.fetch_add(1) == 0 || std::getenv("RS_POLY_JIT_LOG"))
@@ -292,12 +293,17 @@ int sm_count() {
 
 // Units (32 columns each) per CTA for a launch over `total` units: up to kSlicedUnitsPerCta,
 // fewer when that would leave less than ~8 CTAs per SM (single stripes, per-pattern launches).
-uint32_t units_per_cta_for(uint64_t total) {
-  static const uint64_t per_sm = [] {  // tuning knob RS_POLY_CTAS_PER_SM (default 8)
+// Units per CTA so that a launch has about RS_POLY_CTAS_PER_SM CTAs per SM (default 4 for
+// w = 8, 8 for w = 16), in multiples of the CTA size, at most kSlicedUnitsPerCta.  Measured
+// on per-stripe decode chains (r01p): w = 8 (C3, 4 CTAs/SM resident) runs best with 2 units
+// per thread (97% vs 94% of the copy peak with 1, 92% with 4); w = 16 (3 CTAs/SM, a 4x
+// longer body per unit) with 1 (80% vs 68% with 2).
+uint32_t units_per_cta_for(uint64_t total, int w) {
+  static const long env = [] {
     const char *e = std::getenv("RS_POLY_CTAS_PER_SM");
-    const long v = e ? std::strtol(e, nullptr, 10) : 8;
-    return (uint64_t)std::max(1L, std::min(v, 64L));
+    return e ? std::max(1L, std::min(std::strtol(e, nullptr, 10), 64L)) : 0L;
   }();
+  const uint64_t per_sm = env ? (uint64_t)env : (w == 8 ? 4 : 8);
   const uint64_t target = (uint64_t)sm_count() * per_sm;
   uint64_t upc = (total + target - 1) / target;
   upc = (upc + kSlicedThreads - 1) / kSlicedThreads * kSlicedThreads;
@@ -317,7 +323,7 @@ cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32
   a.stripes = stripes;
   a.n_sel = n_sel;
   a.units_per_stripe = body_units;
-  a.units_per_cta = units_per_cta_for(n_sel * body_units);
+  a.units_per_cta = units_per_cta_for(n_sel * body_units, k.w);
   a.ctas_per_stripe = (uint32_t)((body_units + a.units_per_cta - 1) / a.units_per_cta);
   const uint64_t grid = n_sel * a.ctas_per_stripe;
   if (grid == 0) return cudaSuccess;
@@ -352,7 +358,7 @@ cudaError_t launch_sliced_body(const rs_poly_plan &P, bool decode, const Geometr
   a.L = G.L;
   a.n_stripes = G.n_stripes;
   a.units_per_stripe = body_units;
-  a.units_per_cta = units_per_cta_for(G.n_stripes * body_units);
+  a.units_per_cta = units_per_cta_for(G.n_stripes * body_units, P.w);
   a.ctas_per_stripe = (uint32_t)((body_units + a.units_per_cta - 1) / a.units_per_cta);
   if (decode) {
     a.pats = reinterpret_cast<const rsb::SlicedPat *>(dev + pats_off);

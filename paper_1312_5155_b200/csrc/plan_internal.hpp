@@ -294,7 +294,7 @@ const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const JitKey &key, const 
 std::vector<cudaStream_t> side_streams(const rs_poly_plan &P);
 uint64_t body_units_of(const rs_poly_plan &P, const Geometry &G);
 int sm_count();
-uint32_t units_per_cta_for(uint64_t total);
+uint32_t units_per_cta_for(uint64_t total, int w);
 cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32_t *stripes, uint64_t n_sel,
                        uint64_t body_units, cudaStream_t st, bool pdl = false, uint64_t stripe_base = 0,
                        unsigned *flags = nullptr);
