@@ -37,9 +37,11 @@
  * owned device constants) may be captured on the caller's stream once the plan has
  * run once on that device: rs_poly_encode_batch, rs_poly_verify_batch, and
  * rs_poly_decode_batch when every pattern of the batch has its JIT kernel (after
- * rs_poly_prepare), the blocks have no ragged tail and each pattern's stripes are
- * contiguous (e.g. one stripe, one shared pattern, or all patterns distinct).  Calls that upload per-call
- * constants return RS_ERR_CUDA when the stream is capturing (nothing is enqueued).
+ * rs_poly_prepare), the blocks have no ragged tail and the layout is strided (not
+ * the pointer-array form); a pattern recurring on non-adjacent stripes is launched
+ * once per run of adjacent stripes.  Calls that upload per-call constants (ragged
+ * tails, pointer arrays, patterns still without a JIT kernel) return RS_ERR_CUDA
+ * when the stream is capturing (nothing is enqueued).
  * There is no CPU fallback: every entry point that computes runs CUDA kernels.
  */
 #ifndef RS_POLY_H

@@ -718,6 +718,29 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
     hp.mark("launch(lean)");
     return r;
   }
+  // A pattern that recurs on non-adjacent stripes: one lean launch per run of adjacent
+  // stripes instead of a stripe list in an uploaded blob (each CTA would first load its
+  // stripe index from it -- a dependent global load before any of its data loads).
+  // RS_POLY_SPLIT_RUNS=0 keeps the blob path (measurement knob).
+  static const bool split_runs = [] {
+    const char *e = std::getenv("RS_POLY_SPLIT_RUNS");
+    return !(e && e[0] == '0');
+  }();
+  if (split_runs && any_jit && !any_rt && !ptrs && body * UB == G.block_bytes) {
+    std::vector<const rsb::jit::Kernel *> jr;
+    std::vector<std::vector<int32_t>> runs;
+    for (size_t i = 0; i < groups.size(); ++i)
+      for (size_t q = 0; q < groups[i].size(); ++q) {
+        if (q == 0 || groups[i][q] != groups[i][q - 1] + 1) {
+          jr.push_back(jk[i]);
+          runs.emplace_back();
+        }
+        runs.back().push_back(groups[i][q]);
+      }
+    const rs_status r = cuda_status(launch_jit_chains(*P, jr, runs, G, body, nullptr, {}, st));
+    hp.mark("launch(runs)");
+    return r;
+  }
   Blob b;
   size_t ptrs_off = SIZE_MAX;
   if (ptrs) ptrs_off = b.add(ptrs, sizeof(uint64_t) * (size_t)P->n * G.n_stripes);

@@ -69,7 +69,10 @@ def test_prepare_then_decode_uses_only_jit():
     torch.cuda.synchronize()
     assert np.array_equal(d.cpu().numpy(), ref)
     st2 = plan.stats()
-    assert st2["table_launches"] == 0 and st2["jit_launches"] == st["jit_ready"]
+    # one launch per run of adjacent stripes sharing a pattern (nothing uploaded)
+    rows = [tuple(r) for r in er.tolist()]
+    runs = sum(1 for s in range(S) if s == 0 or rows[s] != rows[s - 1])
+    assert st2["table_launches"] == 0 and st2["jit_launches"] == runs
 
 
 def test_background_mode_converges():
@@ -330,11 +333,27 @@ def test_cuda_graph_capture():
     g_dec.replay()
     torch.cuda.synchronize()
     assert np.array_equal(d.cpu().numpy(), ref)
-    # patterns A, B, A, B: A's stripes are not contiguous -> per-call stripe lists to upload
+    # patterns A, B, A, B: one launch per run of adjacent stripes, still nothing uploaded
     er_mixed = np.array([[1, 4, 10, 13], [0, 2, 3, 5], [1, 4, 10, 13], [0, 2, 3, 5]], dtype=np.int32)
     plan.prepare(er_mixed)
+    with torch.cuda.stream(cap):
+        plan.decode_batch(d, er_mixed, stream=cap)
+    torch.cuda.synchronize()
+    g_mixed = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_mixed, stream=cap):
+        plan.decode_batch(d, er_mixed, stream=cap)
+    for s_, row in enumerate(er_mixed):
+        d[s_, list(row)] = 0x5A
+    g_mixed.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    # a ragged block length: the tail kernel reads per-call pattern records -> refused
+    Br = B - 40
+    rag = torch.from_numpy(np.ascontiguousarray(encoded(k, m, 8, P8, Br, S, seed=112))).cuda()
+    plan.decode_batch(rag, er_mixed)
+    torch.cuda.synchronize()
     g_bad = torch.cuda.CUDAGraph()
     with pytest.raises((m_.RSError, RuntimeError)):
         with torch.cuda.graph(g_bad, stream=cap):
-            plan.decode_batch(d, er_mixed, stream=cap)
+            plan.decode_batch(rag, er_mixed, stream=cap)
     torch.cuda.synchronize()
