@@ -38,9 +38,10 @@
  * run once on that device: rs_poly_encode_batch, rs_poly_verify_batch, and
  * rs_poly_decode_batch when every pattern of the batch has its JIT kernel (after
  * rs_poly_prepare), the blocks have no ragged tail and the layout is strided (not
- * the pointer-array form); a pattern recurring on non-adjacent stripes is launched
- * once per run of adjacent stripes.  Calls that upload per-call constants (ragged
- * tails, pointer arrays, patterns still without a JIT kernel) return RS_ERR_CUDA
+ * the pointer-array form) and each pattern's stripes form at most two runs of adjacent
+ * stripes on average (a pattern recurring on non-adjacent stripes is launched once per
+ * run).  Calls that upload per-call constants (ragged tails, pointer arrays, patterns
+ * still without a JIT kernel, patterns scattered over many runs) return RS_ERR_CUDA
  * when the stream is capturing (nothing is enqueued).
  * There is no CPU fallback: every entry point that computes runs CUDA kernels.
  */

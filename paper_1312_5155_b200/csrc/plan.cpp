@@ -726,9 +726,18 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
     const char *e = std::getenv("RS_POLY_SPLIT_RUNS");
     return !(e && e[0] == '0');
   }();
-  if (split_runs && any_jit && !any_rt && !ptrs && body * UB == G.block_bytes) {
+  // Only while that adds few launches: at most twice the patterns' (alternating patterns
+  // over many small stripes would otherwise turn one launch per pattern into one per stripe).
+  size_t n_runs = 0, n_groups = 0;
+  for (const auto &gr : groups) {
+    n_groups += !gr.empty();
+    for (size_t q = 0; q < gr.size(); ++q) n_runs += q == 0 || gr[q] != gr[q - 1] + 1;
+  }
+  if (split_runs && any_jit && !any_rt && !ptrs && body * UB == G.block_bytes && n_runs <= 2 * n_groups) {
     std::vector<const rsb::jit::Kernel *> jr;
     std::vector<std::vector<int32_t>> runs;
+    jr.reserve(n_runs);
+    runs.reserve(n_runs);
     for (size_t i = 0; i < groups.size(); ++i)
       for (size_t q = 0; q < groups[i].size(); ++q) {
         if (q == 0 || groups[i][q] != groups[i][q - 1] + 1) {

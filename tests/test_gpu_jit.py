@@ -357,3 +357,27 @@ def test_cuda_graph_capture():
         with torch.cuda.graph(g_bad, stream=cap):
             plan.decode_batch(rag, er_mixed, stream=cap)
     torch.cuda.synchronize()
+
+
+def test_alternating_patterns_keep_one_launch_per_pattern():
+    """Two patterns alternating over many small stripes: runs of adjacent stripes would be
+    one launch per stripe, so the batch keeps one launch per pattern (stripe lists in the
+    uploaded blob); three patterns in long runs split into one launch per run."""
+    k, m, B, S = 10, 4, 4096, 64
+    ref = encoded(k, m, 8, P8, B, S, seed=113)
+    m_ = rs()
+    plan = m_.Plan(k, m)
+    A, Bp, Cp = [1, 4, 10, 13], [0, 2, 3, 5], [6, 7, 8, 9]
+    for rows, want in (([A if s % 2 == 0 else Bp for s in range(S)], 2),
+                       ([A] * 20 + [Bp] * 20 + [A] * 14 + [Cp] * 10, 4)):
+        er = np.array(rows, dtype=np.int32)
+        plan.prepare(er)
+        bad = ref.copy()
+        for s in range(S):
+            bad[s, er[s]] = 0xEE
+        d = torch.from_numpy(bad).cuda()
+        n0 = plan.stats()["jit_launches"]
+        plan.decode_batch(d, er)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy(), ref)
+        assert plan.stats()["jit_launches"] - n0 == want
