@@ -73,3 +73,46 @@ def test_fuzz_against_oracle(case):
         plan.update_batch(d, idx, old)
         torch.cuda.synchronize()
         assert np.array_equal(d.cpu().numpy(), want), "update"
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_fuzz_pattern_sequences(case):
+    """Batches whose stripes draw their erasure pattern from a small set in random order
+    (runs of adjacent stripes, recurring patterns, patterns still compiling): decode is
+    bit-exact whichever launch plan the batch gets (one launch per pattern, per run, or the
+    table kernel)."""
+    rng = np.random.default_rng(5000 + case)
+    w = int(rng.choice([8, 8, 16]))
+    k, m = (10, 4) if w == 8 else (12, 4)
+    sym = w // 8
+    B = int(rng.choice([4096, 8192, 64 * 1024, int(rng.integers(1, 9000)) // sym * sym or sym]))
+    S = int(rng.integers(2, 48))
+    n = k + m
+    m_ = rs()
+    plan = m_.Plan(k, m, w, POLY[w])
+    plan.set_jit(int(rng.choice([m_.RS_JIT_SYNC, m_.RS_JIT_BACKGROUND])))
+    npat = int(rng.integers(1, 5))
+    pats = [np.sort(rng.choice(n, int(rng.integers(1, m + 1)), replace=False)) for _ in range(npat)]
+    if rng.integers(2):   # runs
+        seq = []
+        while len(seq) < S:
+            seq += [int(rng.integers(npat))] * int(rng.integers(1, 8))
+        seq = seq[:S]
+    else:                 # independent draws
+        seq = [int(rng.integers(npat)) for _ in range(S)]
+    er = np.full((S, m), -1, dtype=np.int32)
+    for s, p in enumerate(seq):
+        er[s, :len(pats[p])] = pats[p]
+    if rng.integers(2):
+        plan.prepare(er)
+    ref = synth.stripes_array(7000 + case, range(S), k, m, B)
+    oracle.encode_bulk(ref, k, m, w, POLY[w], threads=4)
+    bad = ref.copy()
+    for s in range(S):
+        for b in er[s]:
+            if b >= 0:
+                bad[s, b] = 0xA5
+    d = torch.from_numpy(bad).cuda()
+    plan.decode_batch(d, er)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
