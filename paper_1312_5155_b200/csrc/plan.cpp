@@ -147,7 +147,11 @@ rsb::jit::Spec jit_spec(const rs_poly_plan &P, const std::vector<int> &in, const
   s.out_blk = out;
   s.M = M;
   s.group_blocks = P.w == 8 ? 0 : 3;  // w16: CSE groups of 3 blocks keep the planes in registers
-  s.min_blocks = P.w == 8 ? 4 : 3;
+  static const int w8_minb = [] {  // RS_POLY_JIT_W8_MINB (measurement knob, default 4)
+    const char *e = std::getenv("RS_POLY_JIT_W8_MINB");
+    return e ? (int)std::max(1L, std::min(std::strtol(e, nullptr, 10), 8L)) : 4;
+  }();
+  s.min_blocks = P.w == 8 ? w8_minb : 3;
   return s;
 }
 
