@@ -134,9 +134,6 @@ rs_status cuda_status(cudaError_t e) {
 }
 
 
-
-
-
 bool jit_eligible(const rs_poly_plan &P, int n_out) { return P.w == 8 ? n_out <= 8 : n_out <= 4; }
 
 rsb::jit::Spec jit_spec(const rs_poly_plan &P, const std::vector<int> &in, const std::vector<int> &out,
@@ -586,12 +583,6 @@ rs_status collect_patterns(const rs_poly_plan *P, const std::vector<std::vector<
   }
   return RS_OK;
 }
-
-
-
-
-
-
 
 
 const rsb::jit::Kernel *pattern_jit(const rs_poly_plan &P, const PatternHost &ph, const MaskKey &key, bool wait) {
@@ -1060,10 +1051,6 @@ size_t rs_poly_jit_source(const rs_poly_plan *P, const int *erasures, int n_eras
   }
   return s.size();
 }
-
-
-
-
 
 
 rs_status rs_poly_ablation_decode(const rs_poly_plan *P, void *stripes, size_t n_stripes, size_t stripe_stride,
