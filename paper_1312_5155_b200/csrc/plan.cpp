@@ -292,9 +292,7 @@ int sm_count() {
   return v;
 }
 
-// Units (32 columns each) per CTA for a launch over `total` units: up to kSlicedUnitsPerCta,
-// fewer when that would leave less than ~8 CTAs per SM (single stripes, per-pattern launches).
-// Units per CTA so that a launch has about RS_POLY_CTAS_PER_SM CTAs per SM (default 4 for
+// Units (32 columns each) per CTA so that a launch has about RS_POLY_CTAS_PER_SM CTAs per SM (default 4 for
 // w = 8, 8 for w = 16), in multiples of the CTA size, at most kSlicedUnitsPerCta.  Measured
 // on per-stripe decode chains (r01p): w = 8 (C3, 4 CTAs/SM resident) runs best with 2 units
 // per thread (97% vs 94% of the copy peak with 1, 92% with 4); w = 16 (3 CTAs/SM, a 4x
@@ -393,8 +391,6 @@ cudaError_t launch_generic_range(const rs_poly_plan &P, const Geometry &G, uint6
   return rsb::launch_generic(P.w, a, st);
 }
 
-// Copy `bytes` at `src` to device `dst` on stream `s` through one of the plan's pinned
-// slots (reused once its previous copy has completed); pageable only if no slot can be had.
 // Process-wide pool (one per device) for the per-call blobs.  The default pool returns its
 // memory to the driver at every synchronize (release threshold 0), so a call after a
 // synchronize would re-map its blob: ~0.2 ms of host time before the first launch, with the
@@ -430,6 +426,8 @@ cudaError_t blob_pool(cudaMemPool_t *out) {
   return cudaSuccess;
 }
 
+// Copy `bytes` at `src` to device `dst` on stream `s` through one of the plan's pinned
+// slots (reused once its previous copy has completed); pageable only if no slot can be had.
 cudaError_t upload_pinned(const rs_poly_plan &P, void *dst, const void *src, size_t bytes, cudaStream_t s) {
   // At most kMaxSlots pinned slots.  When all are in flight the host is at least that
   // many calls ahead of the GPU, so it waits for the oldest copy instead of allocating:
@@ -590,15 +588,6 @@ const rsb::jit::Kernel *pattern_jit(const rs_poly_plan &P, const PatternHost &ph
   return jit_get(P, JitKey{kJitDecode, key}, [&] { return decoder_spec(P, ph); }, wait);
 }
 
-// The per-pattern JIT kernels of one decode call, one launch per pattern (its stripes).
-// Launches form programmatic-dependent-launch chains: each generated kernel triggers its
-// dependents on entry and waits for its predecessor before exit, so kernel i+1's CTAs
-// fill kernel i's last wave (a C4 stripe is only ~2.3 waves) while completion stays in
-// stream order.  The first kernel of a chain is launched without the attribute, so it
-// never overlaps work queued before the call.  With side streams (side_streams()), the
-// patterns are dealt round-robin over 1 + N chains forked from and joined back to `st`.
-// dev_lists: device base of the per-pattern stripe lists (grp_off), or nullptr when every
-// group is a contiguous stripe range (passed by value).
 // RS_POLY_HOST_PROFILE=1: per-call host time of each decode phase on stderr (diagnostics)
 struct HostProfile {
   bool on;
@@ -621,6 +610,16 @@ struct HostProfile {
   }
 };
 
+// The per-pattern JIT kernels of one decode call, one launch per group (a pattern's stripes,
+// or one run of adjacent stripes).
+// Launches form programmatic-dependent-launch chains: each generated kernel triggers its
+// dependents on entry and waits for its predecessor before exit, so kernel i+1's CTAs
+// fill kernel i's last wave (a C4 stripe is only ~2.3 waves) while completion stays in
+// stream order.  The first kernel of a chain is launched without the attribute, so it
+// never overlaps work queued before the call.  With side streams (side_streams()), the
+// patterns are dealt round-robin over 1 + N chains forked from and joined back to `st`.
+// dev_lists: device base of the per-pattern stripe lists (grp_off), or nullptr when every
+// group is a contiguous stripe range (passed by value).
 cudaError_t launch_jit_chains(const rs_poly_plan &P, const std::vector<const rsb::jit::Kernel *> &jk,
                               const std::vector<std::vector<int32_t>> &groups, const Geometry &G, uint64_t body,
                               const uint8_t *dev_lists, const std::vector<size_t> &grp_off, cudaStream_t st) {
