@@ -144,14 +144,17 @@ rsb::jit::Spec jit_spec(const rs_poly_plan &P, const std::vector<int> &in, const
   s.out_blk = out;
   s.M = M;
   // CSE groups of input blocks (0 = one network over all inputs).  w16: 3 blocks keep the
-  // planes in registers.  w8: all inputs while there are at most 4 outputs; with 5+ outputs
-  // one network spills 150-300 B per thread at 128 registers, groups of 4 blocks none
-  // (r01q, RS(10,6): encode 93% -> 103%, decode 77% -> 93% of the copy peak).
+  // planes in registers.  w8: one network while inputs + outputs fit in 14 blocks of planes
+  // (RS(10,4) decode: 36 B spilled at 128 registers, grouping costs more than it saves);
+  // beyond that it spills 136-300 B per thread, and groups of 10 - outputs blocks spill
+  // nothing for +6-14% LOP3 (r01q: RS(10,6) encode 93% -> 103%, decode 77% -> 92%).
   static const int w8_group = [] {  // RS_POLY_JIT_W8_GROUP overrides (measurement knob)
     const char *e = std::getenv("RS_POLY_JIT_W8_GROUP");
     return e ? (int)std::max(0L, std::min(std::strtol(e, nullptr, 10), 64L)) : -1;
   }();
-  s.group_blocks = P.w == 8 ? (w8_group >= 0 ? w8_group : (out.size() > 4 ? 4 : 0)) : 3;
+  const int n_io = (int)(in.size() + out.size());
+  const int w8_auto = n_io > 14 ? std::max(2, 10 - (int)out.size()) : 0;
+  s.group_blocks = P.w == 8 ? (w8_group >= 0 ? w8_group : w8_auto) : 3;
   // w8 at 4 CTAs/SM (128 registers): 3 CTAs/SM without spills is slower even for 5-6
   // outputs (r01q: RS(10,5) encode 88% vs 105%).
   static const int w8_minb = [] {  // RS_POLY_JIT_W8_MINB (measurement knob, default 4)
