@@ -99,6 +99,18 @@ __device__ __forceinline__ void transpose8(uint32_t *x) {
   for (int i = 0; i < 8; i += 2) delta_swap<1, 0x55555555u>(x[i], x[i + 1]);
 }
 
+// The same swap with plain shifts: ptxas puts the left shift on the FMA pipe (IMAD.SHL) and the
+// right one on the ALU pipe (SHF.R) instead of the quarter-rate IMAD.HI.  The w16 kernels
+// (ALU-heavier, power-capped) run faster this way -- C4 encode 91-92% vs 88-90% of the copy
+// peak -- while the w8 decode chains lose 1-4% (profiles/r01r_shift_pipes.log).
+template <int S, uint32_t MASK>
+__device__ __forceinline__ void delta_swap_shf(uint32_t &a, uint32_t &c) {
+  const uint32_t na = bitsel<MASK>(a, c << S);
+  const uint32_t nc = bitsel<MASK>(a >> S, c);
+  a = na;
+  c = nc;
+}
+
 // 16 words (32 columns of LE uint16; word i = columns 2i, 2i+1) <-> 16 planes
 // (plane b = bit b; column 2i+r at plane bit 16r+i).  The byte stage uses PRMT.
 __device__ __forceinline__ void transpose16(uint32_t *x) {
@@ -110,12 +122,12 @@ __device__ __forceinline__ void transpose16(uint32_t *x) {
   }
 #pragma unroll
   for (int i = 0; i < 16; ++i)
-    if ((i & 4) == 0) delta_swap<4, 0x0F0F0F0Fu>(x[i], x[i + 4]);
+    if ((i & 4) == 0) delta_swap_shf<4, 0x0F0F0F0Fu>(x[i], x[i + 4]);
 #pragma unroll
   for (int i = 0; i < 16; ++i)
-    if ((i & 2) == 0) delta_swap<2, 0x33333333u>(x[i], x[i + 2]);
+    if ((i & 2) == 0) delta_swap_shf<2, 0x33333333u>(x[i], x[i + 2]);
 #pragma unroll
-  for (int i = 0; i < 16; i += 2) delta_swap<1, 0x55555555u>(x[i], x[i + 1]);
+  for (int i = 0; i < 16; i += 2) delta_swap_shf<1, 0x55555555u>(x[i], x[i + 1]);
 }
 
 template <int W>
