@@ -349,7 +349,7 @@ cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32
   if (!pdl || !pdl_on)
     return cudaLaunchKernel(reinterpret_cast<const void *>(k.fn), dim3((unsigned)grid), dim3(kSlicedThreads), args,
                             0, st);
-  // programmatic dependent launch (the generated kernels trigger at entry and wait at exit)
+  // programmatic dependent launch (the generated kernels trigger at entry; their last CTA waits at exit)
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -626,7 +626,7 @@ struct HostProfile {
 // The per-pattern JIT kernels of one decode call, one launch per group (a pattern's stripes,
 // or one run of adjacent stripes).
 // Launches form programmatic-dependent-launch chains: each generated kernel triggers its
-// dependents on entry and waits for its predecessor before exit, so kernel i+1's CTAs
+// dependents on entry and its last CTA waits for the predecessor before exit, so kernel i+1's CTAs
 // fill kernel i's last wave (a C4 stripe is only ~2.3 waves) while completion stays in
 // stream order.  The first kernel of a chain is launched without the attribute, so it
 // never overlaps work queued before the call.  With side streams (side_streams()), the
