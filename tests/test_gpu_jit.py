@@ -381,3 +381,30 @@ def test_alternating_patterns_keep_one_launch_per_pattern():
         torch.cuda.synchronize()
         assert np.array_equal(d.cpu().numpy(), ref)
         assert plan.stats()["jit_launches"] - n0 == want
+
+
+@pytest.mark.parametrize("w", [8, 16])
+def test_pdl_chain_completes_in_stream_order(w):
+    """A decode call is a chain of per-pattern launches in which only each kernel's last CTA
+    waits for its predecessor.  Work queued after the call on the same stream (here an
+    asynchronous copy to pinned host memory) must still see every kernel's output: repeated
+    calls with short kernels and many patterns, each followed at once by the copy."""
+    k, m, poly = (10, 4, P8) if w == 8 else (12, 4, P16)
+    B, S = 16 * 1024, 96
+    ref = encoded(k, m, w, poly, B, S, seed=120 + w)
+    m_ = rs()
+    plan = m_.Plan(k, m, w, poly)
+    d = torch.from_numpy(ref).cuda()
+    host = torch.empty(d.shape, dtype=torch.uint8).pin_memory()
+    rng = np.random.default_rng(w)
+    stream = torch.cuda.current_stream()
+    pats = np.array([np.sort(rng.choice(k + m, m, replace=False)) for _ in range(S)], dtype=np.int32)
+    plan.prepare(pats)                                 # compiled once; each rep reorders them
+    for rep in range(8):
+        er = np.ascontiguousarray(pats[rng.permutation(S)])
+        for s in range(S):
+            d[s, list(er[s])] = 0xEE                   # queued on the same stream
+        plan.decode_batch(d, er)
+        host.copy_(d, non_blocking=True)
+        stream.synchronize()
+        assert np.array_equal(host.numpy(), ref), rep
