@@ -57,6 +57,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample duration")
     ap.add_argument("--jit", default="on", choices=["on", "off"], help="per-pattern JIT decode kernels")
+    ap.add_argument("--verify", default="full", choices=["full", "sampled"],
+                    help="oracle check before timing: every stripe (default) or stripes 0, S/2, S-1")
     return ap.parse_args()
 
 
@@ -87,13 +89,35 @@ def copy_peak_in_run(dev) -> float:
     return 2 * (1 << 30) * 2 / (best / 1e3) / 1e9
 
 
+LIB_SOURCES = ("paper_1312_5155_b200/csrc", "include")
+
+
+def code_hash() -> str:
+    """sha256 (16 hex digits) of the library's sources: kernels, planner, JIT generator and the
+    ABI header -- the code an ncu traffic capture is valid for."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in LIB_SOURCES:
+        base = os.path.join(ROOT, d)
+        for name in sorted(os.listdir(base)):
+            if name.endswith((".cu", ".cuh", ".cpp", ".hpp", ".h", ".py")):
+                h.update(name.encode())
+                with open(os.path.join(base, name), "rb") as f:
+                    h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def ncu_traffic(cfg: str, op: str):
-    """DRAM bytes per call of the dominant kernel from the committed ncu capture (or None)."""
+    """(DRAM bytes per call, source note) of one whole call from the committed ncu capture
+    (tools/ncu_traffic.py); (None, why) unless it was taken on this exact library source."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return int(json.load(f)[cfg][op]["bytes_per_call"])
+            e = json.load(f)[cfg][op]
     except Exception:
-        return None
+        return None, "no capture for this config"
+    if e.get("code_hash") != code_hash():
+        return None, f"capture is of code {e.get('code_hash')}, not this build ({code_hash()}): refused"
+    return int(e["bytes_per_call"]), e.get("source", "")
 
 
 def allreduce(x: float, op: str, world: int, device) -> float:
@@ -136,37 +160,69 @@ def oracle_pass(oracle, st, er, c, threads):
     oracle.decode_bulk(st, er, c["k"], c["m"], c["w"], c["poly"], threads=threads)
 
 
-def cpu_baseline(c, seconds: float):
+def cpu_model() -> str:
+    """The host CPU's model string (/proc/cpuinfo), for the baseline's context (P:361 states the paper's)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def core_partition(local_rank: int, local_world: int) -> list[int]:
+    """This rank's share of the node's host cores: the process affinity split into
+    local_world contiguous slices (the ranks of one node share its cores)."""
+    cpus = sorted(os.sched_getaffinity(0))
+    per = max(1, len(cpus) // max(1, local_world))
+    lo = min(local_rank * per, max(0, len(cpus) - per))
+    return cpus[lo:lo + per]
+
+
+def cpu_baseline(c, seconds: float, cpus: list[int] | None = None):
+    """The oracle (as it stands) on host cores: `cpus` (default: all of this process's), one
+    thread per core and per stripe, on a bounded prefix of the config's stripes."""
     import oracle
-    cores = os.cpu_count() or 1
-    threads = max(1, min(cores, c["stripes"]))
-    prefix = min(c["block_bytes"], 2 << 20)
-    st, er = oracle_sample(c, threads, prefix)
-    oracle_pass(oracle, st, er, c, threads)  # warm
-    passes, t0 = 0, time.perf_counter()
-    while True:
-        oracle_pass(oracle, st, er, c, threads)
-        passes += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
-            break
-    user = threads * c["k"] * prefix
-    # single thread, one stripe: the paper's per-core framing
-    st1, er1 = oracle_sample(c, 1, prefix)
-    p1, t1 = 0, time.perf_counter()
-    while True:
-        oracle_pass(oracle, st1, er1, c, 1)
-        p1 += 1
-        e1 = time.perf_counter() - t1
-        if e1 >= seconds / 4:
-            break
+    old_aff = os.sched_getaffinity(0)
+    if cpus:
+        os.sched_setaffinity(0, cpus)
+    try:
+        cores = len(os.sched_getaffinity(0))
+        threads = max(1, min(cores, c["stripes"]))
+        prefix = min(c["block_bytes"], 2 << 20)
+        st, er = oracle_sample(c, threads, prefix)
+        oracle_pass(oracle, st, er, c, threads)  # warm
+        passes, t0 = 0, time.perf_counter()
+        while True:
+            oracle_pass(oracle, st, er, c, threads)
+            passes += 1
+            el = time.perf_counter() - t0
+            if el >= seconds:
+                break
+        user = threads * c["k"] * prefix
+        # single thread, one stripe: the paper's per-core framing (BASELINE.md section 3)
+        st1, er1 = oracle_sample(c, 1, prefix)
+        p1, t1 = 0, time.perf_counter()
+        while True:
+            oracle_pass(oracle, st1, er1, c, 1)
+            p1 += 1
+            e1 = time.perf_counter() - t1
+            if e1 >= seconds / 4:
+                break
+    finally:
+        os.sched_setaffinity(0, old_aff)
     single = {"value": round(2 * c["k"] * prefix * p1 / e1 / 1e9, 4), "unit": "GB/s", "cores": 1,
               "sample": f"1 stripe x {c['k']} data blocks x first {prefix} B, {p1} passes in {e1:.1f} s"}
     return {"value": round(2 * user * passes / el / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "threads": threads, "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
             "single_thread": single,
             "sample": f"{threads} stripes x {c['k']} data blocks x first {prefix} B of each block "
                       f"({user / 2**20:.0f} MiB user data), encode + decode with the config's erasure patterns, "
-                      f"{passes} passes in {el:.1f} s, {threads} threads (one stripe each) of {cores} host cores"}
+                      f"{passes} passes in {el:.1f} s, {threads} threads (one stripe each) on {cores} of "
+                      f"{os.cpu_count()} host cores ({cpu_model()})"}
 
 
 def run_reference(args):
@@ -188,7 +244,7 @@ def run_reference(args):
     user = threads * c["k"] * prefix
     value = 2 * user * args.steps / el / 1e9
     sample = (f"per step: {threads} stripes x {c['k']} data blocks x first {prefix} B of each block of the "
-              f"{args.config} workload, encode + decode; {threads} threads")
+              f"{args.config} workload, encode + decode; {threads} threads of {cores} host cores ({cpu_model()})")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
@@ -198,7 +254,7 @@ def run_reference(args):
                    "prim_poly": hex(c["poly"]), "block_bytes": c["block_bytes"], "stripes_per_gpu": c["stripes"],
                    "parallelism": f"dp{args.gpus}"},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
-                         "sample": sample},
+                         "threads": threads, "cpu_model": cpu_model(), "host_cpus": cores, "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -318,19 +374,30 @@ def run_ours(args):
     plan.prepare(er)
     setup_ms = (time.perf_counter() - t_setup) * 1e3
 
-    # ---- correctness before any number: encode vs the oracle on sampled columns,
-    # and decode restores every byte of every stripe (exact compare on device) ----
+    # ---- correctness before any number: every byte of every stripe vs the CPU oracle ----
+    # (outside the timed region, MDS uniqueness P:33).  At N > 1 the ranks
+    # share the node's cores, so rank r checks its stripes s = r (mod N): S stripes of
+    # host work in total, as at N = 1.
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    vcpus = core_partition(local, local_world) if world > 1 else sorted(os.sched_getaffinity(0))
+    vids = list(range(S)) if world == 1 else [s for s in range(S) if s % world == rank % world]
+    if args.verify == "sampled":
+        vids = sorted({0, S // 2, S - 1})
+
+    def fetch(ids):
+        return np.stack([stripes[s_].cpu().numpy() for s_ in ids])
+
     plan.encode_batch(stripes)
     torch.cuda.synchronize()
-    mismatches = verify_encode_sampled(stripes, c)
+    checks = verify_full(fetch, c, er, vids, vcpus, phase="encode")
     golden = stripes.clone()
     for s in range(S):
         stripes[s].index_fill_(0, er_t[s], 0xEE)
     plan.decode_batch(stripes, er)
     torch.cuda.synchronize()
-    mismatches += 0 if torch.equal(stripes, golden) else 1
-    del golden
-    torch.cuda.empty_cache()
+    checks += verify_full(fetch, c, er, vids, vcpus, phase="decode")
+    roundtrip_ok = torch.equal(stripes, golden)
+    mismatches = sum(len(ch["mismatched_stripes"]) for ch in checks) + (0 if roundtrip_ok else 1)
 
     # ---- warm-up ----
     for _ in range(args.warmup):
@@ -360,11 +427,14 @@ def run_ours(args):
     total_ms = allreduce(total_ms, "max", world, dev)
     enc_avg, dec_avg = statistics.mean(enc_ms), statistics.mean(dec_ms)
 
-    # post-run check: the timed passes reproduced the verified batch
-    plan.encode_batch(stripes)
-    torch.cuda.synchronize()
-    mismatches += verify_encode_sampled(stripes, c)
+    # post-run check: the timed passes (ending with a decode) left exactly the verified batch
+    after_ok = torch.equal(stripes, golden)
+    del golden
+    torch.cuda.empty_cache()
+    mismatches += 0 if after_ok else 1
     mismatches = int(allreduce(float(mismatches), "sum", world, dev))
+    verified_bytes = int(allreduce(float(sum(ch["bytes"] for ch in checks if ch["phase"] == "decode")), "sum",
+                                   world, dev))
 
     user_bytes = S * k * B                      # per GPU per pass
     moved = S * (k + m) * B                     # HBM bytes per pass (read once or written once)
@@ -375,7 +445,7 @@ def run_ours(args):
     dec_kernel = "rs_jit (per-pattern NVRTC XOR network)" if jst["jit_launches"] else "sliced_kernel decode (tables)"
     dom_ms, dom_name = (dec_avg, "decode: " + dec_kernel) if dec_avg >= enc_avg else (enc_avg, "encode: sliced_kernel")
     achieved = moved / (dom_ms / 1e3) / 1e9
-    traffic = ncu_traffic(args.config, "decode" if dom_name.startswith("decode") else "encode")
+    traffic, traffic_src = ncu_traffic(args.config, "decode" if dom_name.startswith("decode") else "encode")
 
     # ---- end to end through the public API from pinned host memory ----
     e2e = None
@@ -383,8 +453,23 @@ def run_ours(args):
         e2e = run_e2e(args, plan, stripes, er, c, world, dev, barrier)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(c, args.cpu_seconds)
+    if not args.no_cpu_baseline:
+        if world == 1:
+            cpu = cpu_baseline(c, args.cpu_seconds)
+        else:  # every rank on its own slice of the node's cores, concurrently
+            part = core_partition(local, local_world)
+            mine = cpu_baseline(c, args.cpu_seconds, cpus=part)
+            mine.update(rank=rank, cpus=f"{part[0]}-{part[-1]}")
+            per_rank = [None] * world
+            dist.all_gather_object(per_rank, mine)
+            cpu = {"value": round(sum(r_["value"] for r_ in per_rank), 4), "unit": "GB/s",
+                   "cores": sum(r_["cores"] for r_ in per_rank), "kind": "oracle",
+                   "threads": sum(r_["threads"] for r_ in per_rank), "cpu_model": cpu_model(),
+                   "host_cpus": os.cpu_count(),
+                   "sample": f"each of the {world} ranks ran the oracle on its own core slice at the same time "
+                             f"({per_rank[0]['sample']}); value = sum over ranks",
+                   "per_rank": [{k_: r_[k_] for k_ in ("rank", "cpus", "cores", "value", "single_thread")}
+                                for r_ in per_rank]}
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": K,
@@ -396,7 +481,9 @@ def run_ours(args):
                    "kernels": plan.kernel_kind,
                    "l2": f"inputs {S * n * B / 2**30:.1f} GiB per GPU >> 126 MB L2: no flush needed"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                     "traffic_over_algorithmic": round(traffic / moved, 4) if traffic else None,
+                     "code_hash": code_hash(),
                      "kernel": f"{dom_name}; {moved} algorithmic bytes per call = S*(k+m)*B, avg {dom_ms:.4f} ms",
                      "peak_source": peak_src,
                      "peak_in_run": round(peak_run, 1), "frac_in_run": round(achieved / peak_run, 4),
@@ -408,8 +495,15 @@ def run_ours(args):
                    "hbm_frac": round(moved / (dec_avg / 1e3) / 1e9 / peak, 4),
                    "ms_min_med_max": [round(min(dec_ms), 4), round(statistics.median(dec_ms), 4), round(max(dec_ms), 4)]},
         "verified": {"mismatches": mismatches,
-                     "how": "encode vs CPU oracle on sampled columns of 3 stripes (before and after timing); "
-                            "decode restores all S*n*B bytes (exact device compare)"},
+                     "how": (f"all S*n*B bytes vs oracle: every byte of {'every stripe' if args.verify == 'full' else 'stripes ' + str(vids)}"
+                             f"{' (rank r: stripes = r mod N)' if world > 1 and args.verify == 'full' else ''} "
+                             "compared with the CPU oracle's encode (oracle/rs_oracle.c long division of the "
+                             "synth data) after the device encode, and with the oracle's own decode of the same "
+                             "erasures after the device decode; plus device round trip and the batch after "
+                             "the timed passes equal to that verified state"),
+                     "oracle_bytes_compared_per_phase": verified_bytes,
+                     "checks": [{k_: v for k_, v in ch.items() if k_ != "mismatched_stripes"} |
+                                {"mismatched": len(ch["mismatched_stripes"])} for ch in checks]},
         "gpu_launches": launches,
         "setup": {"ms": round(setup_ms, 1), "what": "rs_poly_prepare: decode constants + JIT kernels for the "
                   "batch's erasure patterns (once per pattern, outside the timed region)",
@@ -427,20 +521,21 @@ def run_ours(args):
     return 0 if mismatches == 0 else 1
 
 
-def verify_encode_sampled(stripes, c) -> int:
-    """Oracle re-encode of sampled columns (first/last 64 KiB of every block) of stripes 0, S/2, S-1."""
-    import oracle
-    k, m, n, w, B, S = c["k"], c["m"], c["n"], c["w"], c["block_bytes"], c["stripes"]
-    span = min(B // 2, 64 << 10) // (w // 8) * (w // 8)
-    bad = 0
-    for s in sorted({0, S // 2, S - 1}):
-        host = synth.stripes_array(c["seed"], [s], k, m, B)
-        cols = np.concatenate([host[:, :, :span], host[:, :, B - span:]], axis=2).copy()
-        oracle.encode_bulk(cols, k, m, w, c["poly"], threads=2)
-        got = stripes[s].cpu().numpy()
-        got = np.concatenate([got[None, :, :span], got[None, :, B - span:]], axis=2)
-        bad += int(not np.array_equal(got, cols))
-    return bad
+def verify_full(fetch, c, er, ids, cpus, phase: str) -> list[dict]:
+    """Bit-exact check of stripes `ids` against the oracle (oracle/fullcheck.py) on `cpus`."""
+    from oracle import fullcheck
+    old = os.sched_getaffinity(0)
+    os.sched_setaffinity(0, cpus)
+    try:
+        if phase == "encode":
+            r = fullcheck.check_encode(fetch, c, ids, threads=len(cpus))
+        else:
+            r = fullcheck.check_decode(fetch, c, er, ids, threads=len(cpus))
+    finally:
+        os.sched_setaffinity(0, old)
+    r["phase"] = phase
+    r["threads"] = len(cpus)
+    return [r]
 
 
 def gpu_local_cpus(index: int):
@@ -520,8 +615,38 @@ def _run_e2e(K, plan, stripes, er, S, k, B, world, dev, barrier, local, n_all):
                    "device->host outputs inside the timed region (wall clock, max over ranks)"}
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args) -> int | None:
+    """One process per GPU.  Under a launcher (WORLD_SIZE set) --gpus must match the world
+    size; without one, --gpus N > 1 re-executes this command under torch.distributed.run
+    (N ranks on this node, rendezvous on 127.0.0.1) and returns its exit code."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world} (one rank per GPU): refusing to run",
+                  file=sys.stderr, flush=True)
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print("bench.py: launching", " ".join(cmd[1:]), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    rc = launch_ranks(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

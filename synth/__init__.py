@@ -56,13 +56,25 @@ def data_block(seed: int, stripe: int, block: int, block_bytes: int) -> np.ndarr
     return splitmix64(ctr).view(np.uint8)[:block_bytes].copy()
 
 
-def stripes_array(seed: int, stripe_ids, k: int, m: int, block_bytes: int) -> np.ndarray:
-    """``[len(stripe_ids)][k+m][block_bytes]`` uint8 with data filled, parity zeroed."""
+def stripes_array(seed: int, stripe_ids, k: int, m: int, block_bytes: int, threads: int = 1) -> np.ndarray:
+    """``[len(stripe_ids)][k+m][block_bytes]`` uint8 with data filled, parity zeroed.
+
+    ``threads`` > 1 fills the blocks from a thread pool (numpy's ufunc loops release the GIL)."""
     stripe_ids = list(stripe_ids)
     out = np.zeros((len(stripe_ids), k + m, block_bytes), dtype=np.uint8)
-    for si, s in enumerate(stripe_ids):
-        for j in range(k):
-            out[si, j] = data_block(seed, s, j, block_bytes)
+    jobs = [(si, s, j) for si, s in enumerate(stripe_ids) for j in range(k)]
+
+    def fill(job):
+        si, s, j = job
+        out[si, j] = data_block(seed, s, j, block_bytes)
+
+    if threads > 1 and len(jobs) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(threads, len(jobs))) as ex:
+            list(ex.map(fill, jobs))
+    else:
+        for job in jobs:
+            fill(job)
     return out
 
 

@@ -80,19 +80,59 @@ def test_reference_arm_under_torchrun_prints_once():
     assert np.isfinite(d["ms_per_step"])
 
 
-def test_bench_verification_catches_one_flipped_byte():
-    """T6 negative test of the harness: bench.py's oracle check of sampled columns reports a
-    single corrupted parity byte (CPU tensors; the check itself is host-side)."""
-    import torch
+def test_bench_full_verification_catches_one_flipped_byte():
+    """T6 negative test of the harness: bench.py's whole-batch oracle check (oracle/fullcheck.py)
+    reports a single corrupted byte anywhere in a stripe, after encode and after decode (CPU
+    arrays stand in for the device copies; the check itself is host-side)."""
     sys.path.insert(0, ROOT)
     import bench
     import oracle
     import synth
     c = bench.workload("C1", 0)
     c["stripes"] = 3
-    st = synth.stripes_array(c["seed"], range(3), c["k"], c["m"], c["block_bytes"])
-    oracle.encode_bulk(st, c["k"], c["m"], c["w"], c["poly"], threads=2)
-    t = torch.from_numpy(st)
-    assert bench.verify_encode_sampled(t, c) == 0
-    t[1, c["k"] + 2, 17] ^= 0x01            # inside the sampled first 32 KiB of stripe S/2
-    assert bench.verify_encode_sampled(t, c) == 1
+    c["block_bytes"] = 4096 + 40          # a ragged length
+    er = synth.erasure_table("C1", 0, 3)
+    good = synth.stripes_array(c["seed"], range(3), c["k"], c["m"], c["block_bytes"])
+    oracle.encode_bulk(good, c["k"], c["m"], c["w"], c["poly"], threads=2)
+    cpus = sorted(os.sched_getaffinity(0))
+    ids = [0, 1, 2]
+    for phase in ("encode", "decode"):
+        dev = good.copy()
+        r = bench.verify_full(lambda q: dev[q], c, er, ids, cpus, phase)[0]
+        assert r["mismatched_stripes"] == [] and r["bytes"] == good.nbytes
+        dev[1, c["k"] + 2, 4100] ^= 0x01      # one parity byte in the tail of stripe 1
+        r = bench.verify_full(lambda q: dev[q], c, er, ids, cpus, phase)[0]
+        assert r["mismatched_stripes"] == [1]
+
+
+def test_bench_self_launches_ranks_for_gpus_n():
+    """`bench.py --gpus 2` without an outside launcher re-executes itself under
+    torch.distributed.run: one JSON line from rank 0 with n_gpus 2."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+           "--warmup", "0", "--config", "C5"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2"
+    assert d["cpu_baseline"]["cpu_model"] and d["cpu_baseline"]["threads"] >= 1
+
+
+def test_bench_refuses_gpus_world_size_mismatch():
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0")
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=120, env=env, cwd=ROOT)
+    assert p.returncode != 0 and "WORLD_SIZE=3" in p.stderr and not p.stdout.strip()
+
+
+def test_core_partition_slices_the_node():
+    import bench
+    cpus = sorted(os.sched_getaffinity(0))
+    parts = [bench.core_partition(r, 2) for r in range(2)]
+    if len(cpus) >= 2:
+        assert set(parts[0]).isdisjoint(parts[1]) and len(parts[0]) == len(cpus) // 2
+    assert all(p and set(p) <= set(cpus) for p in parts)
+    assert bench.cpu_model()

@@ -9,7 +9,7 @@
   printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
 
 constexpr int ITERS = 4096;
-constexpr int CH = 8;  // independent chains per thread
+constexpr int CH = 12;  // independent chains per thread
 
 __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r; asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r;
@@ -27,8 +27,17 @@ __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {
   uint32_t r; asm volatile("mul.hi.u32 %0, %1, 268435456;" : "=r"(r) : "r"(a)); return r ^ 0 * b;
 }
 
+// right shift by S as the high word of a 32x32->64 product with a multiplier ptxas cannot see
+// (a kernel argument): IMAD.WIDE.U32 on the FMA pipe instead of SHF.R on the ALU pipe
+__device__ __forceinline__ uint32_t mulwide_hi(uint32_t a, uint32_t mul) {
+  uint64_t r; asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(mul)); return (uint32_t)(r >> 32);
+}
+__device__ __forceinline__ uint32_t mulhi_reg(uint32_t a, uint32_t mul) {
+  uint32_t r; asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(mul)); return r;
+}
+
 template <int OP>
-__global__ void pipe_kernel(uint32_t *out, long long *cyc, uint32_t seed) {
+__global__ void pipe_kernel(uint32_t *out, long long *cyc, uint32_t seed, uint32_t mul) {
   uint32_t x[CH], y = seed ^ threadIdx.x, z = seed * 3u + blockIdx.x;
 #pragma unroll
   for (int c = 0; c < CH; ++c) x[c] = seed + c * 77u + threadIdx.x;
@@ -44,6 +53,12 @@ __global__ void pipe_kernel(uint32_t *out, long long *cyc, uint32_t seed) {
       if (OP == 4) x[c] = mulhi(x[c], y);
       if (OP == 5) { x[c] = (c & 1) ? imadshl(x[c], y) : lop3(x[c], y, z); }  // half FMA, half ALU
       if (OP == 6) { x[c] = lop3(x[c], y, z); x[c] = imadshl(x[c], z); }       // 1:1 dependent
+      if (OP == 8) x[c] = mulwide_hi(x[c], mul);
+      if (OP == 9) x[c] = mulhi_reg(x[c], mul);
+      if (OP == 10) { x[c] = (c & 1) ? mulwide_hi(x[c], mul) : lop3(x[c], y, z); }  // 1:1 indep
+      if (OP == 11) { x[c] = (c % 3 == 2) ? mulwide_hi(x[c], mul) : lop3(x[c], y, z); }  // 2 ALU : 1
+      if (OP == 12) { x[c] = (c % 3 == 2) ? mulhi(x[c], y) : lop3(x[c], y, z); }  // 2 ALU : 1 IMAD.HI
+      if (OP == 13) { x[c] = (c & 3) == 3 ? mulwide_hi(x[c], mul) : ((c & 3) == 2 ? imadshl(x[c], y) : lop3(x[c], y, z)); }
     }
   }
   __syncthreads();
@@ -107,27 +122,35 @@ int main() {
   const int SM = p.multiProcessorCount, TPB = 1024;
   uint32_t *out; long long *cyc; CK(cudaMalloc(&out, SM * 4 * TPB * 4)); CK(cudaMalloc(&cyc, SM * 4 * 8));
   long long hc[1024];
-  const char *names[] = {"lop3", "shf", "prmt", "imad.shl", "mul.hi", "lop3+imad(1:1 indep)", "lop3->imad dep"};
+  const char *names[] = {"lop3", "shf", "prmt", "imad.shl", "mul.hi", "lop3+imad(1:1 indep)", "lop3->imad dep", "lds",
+                         "mul.wide hi (reg)", "mul.hi (reg)", "lop3+mul.wide(1:1)", "lop3+mul.wide(2:1)",
+                         "lop3+mul.hi(2:1)", "lop3:shl:mulwide 2:1:1"};
   auto run = [&](int op) {
     for (int rep = 0; rep < 2; ++rep) {
       switch (op) {
-        case 0: pipe_kernel<0><<<SM, TPB>>>(out, cyc, 7); break;
-        case 1: pipe_kernel<1><<<SM, TPB>>>(out, cyc, 7); break;
-        case 2: pipe_kernel<2><<<SM, TPB>>>(out, cyc, 7); break;
-        case 3: pipe_kernel<3><<<SM, TPB>>>(out, cyc, 7); break;
-        case 4: pipe_kernel<4><<<SM, TPB>>>(out, cyc, 7); break;
-        case 5: pipe_kernel<5><<<SM, TPB>>>(out, cyc, 7); break;
-        case 6: pipe_kernel<6><<<SM, TPB>>>(out, cyc, 7); break;
+        case 0: pipe_kernel<0><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 1: pipe_kernel<1><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 2: pipe_kernel<2><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 3: pipe_kernel<3><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 4: pipe_kernel<4><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 5: pipe_kernel<5><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 6: pipe_kernel<6><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
         case 7: lds_kernel<<<SM, TPB>>>(out, cyc); break;
+        case 8: pipe_kernel<8><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 9: pipe_kernel<9><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 10: pipe_kernel<10><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 11: pipe_kernel<11><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 12: pipe_kernel<12><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
+        case 13: pipe_kernel<13><<<SM, TPB>>>(out, cyc, 7, 1u << 28); break;
       }
     }
     cudaDeviceSynchronize();
     cudaMemcpy(hc, cyc, SM * 8, cudaMemcpyDeviceToHost);
     double mx = 0; for (int i = 0; i < SM; ++i) mx = hc[i] > mx ? hc[i] : mx;
     double ops = (double)TPB * ITERS * CH * (op == 6 ? 2 : 1);
-    printf("%-22s %.1f thread-ops/clk/SM (max block cycles %.0f)\n", op == 7 ? "lds.32" : names[op], ops / mx, mx);
+    printf("%-24s %.1f thread-ops/clk/SM (max block cycles %.0f)\n", op == 7 ? "lds.32" : names[op], ops / mx, mx);
   };
-  for (int op = 0; op <= 7; ++op) run(op);
+  for (int op = 0; op <= 13; ++op) run(op);
 
   // HBM streaming
   size_t bytes = (size_t)4 << 30; void *a, *b; CK(cudaMalloc(&a, bytes)); CK(cudaMalloc(&b, bytes));
