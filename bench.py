@@ -637,7 +637,7 @@ def launch_ranks(args) -> int | None:
         return None
     import subprocess
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(sys.argv[0])] + sys.argv[1:]
     print("bench.py: launching", " ".join(cmd[1:]), file=sys.stderr, flush=True)
     return subprocess.call(cmd)
 

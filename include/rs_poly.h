@@ -253,6 +253,15 @@ rs_status rs_poly_plan_set_read_policy(rs_poly_plan *plan, int policy);
  * table-driven kernels; see rs_poly_plan_stats). */
 rs_status rs_poly_prepare(const rs_poly_plan *plan, const int32_t *erasures, size_t n_rows);
 
+/* rs_poly_prepare for EVERY erasure pattern of 1..max_t blocks (sum_t C(n,t) patterns:
+ * 1470 for RS(10,4) with max_t = 4, 2516 for RS(12,4)): the paper's "once per pattern"
+ * precomputation (Opt1/Opt3) done up front, so that no later decode call
+ * ever runs a pattern on the slower table kernels while its JIT kernel compiles.
+ * Blocks until every kernel is compiled (or loaded from the on-disk cubin cache).
+ * max_t in [0, m] (0 = nothing to do); returns RS_ERR_INVALID_ARG when the count
+ * exceeds max_patterns or the plan's JIT module limit (8192); nothing is prepared then. */
+rs_status rs_poly_prepare_all(const rs_poly_plan *plan, int max_t, size_t max_patterns);
+
 typedef struct {
   uint64_t patterns;       /* decode patterns in the cache                        */
   uint64_t jit_ready;      /* JIT kernels compiled and loaded                     */

@@ -498,8 +498,23 @@ rs_status check_geometry(const rs_poly_plan *P, size_t block_bytes) {
   return RS_OK;
 }
 
+// Plan-static device constants (uploaded once per plan and device).  A pageable cudaMemcpy
+// may return before its DMA lands and runs on the legacy stream, which a non-blocking
+// caller stream does not wait for: the copy is completed (legacy stream synchronized)
+// before the pointer is published, so any later launch on any stream reads it whole.
+uint8_t *upload_plan_consts(const std::vector<uint8_t> &h) {
+  uint8_t *d = nullptr;
+  if (cudaMalloc(reinterpret_cast<void **>(&d), h.size()) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaStreamSynchronize(cudaStreamLegacy) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  return d;
+}
+
 // Device copy of the encode tail constants [GenericPat | tables], made once per plan and
-// device (synchronous upload: later calls on any stream see it).
+// device (upload_plan_consts: complete before first use on any stream).
 const uint8_t *enc_consts(const rs_poly_plan &P) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -511,13 +526,8 @@ const uint8_t *enc_consts(const rs_poly_plan &P) {
   gp.table_off = 0;
   std::memcpy(h.data(), &gp, sizeof(gp));
   std::memcpy(h.data() + kEncTablesOff, P.enc_tab.data(), P.enc_tab.size());
-  uint8_t *d = nullptr;
-  if (cudaMalloc(reinterpret_cast<void **>(&d), h.size()) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-    cudaFree(d);
-    return nullptr;
-  }
-  P.enc_dev.emplace(dev, d);
+  uint8_t *d = upload_plan_consts(h);
+  if (d) P.enc_dev.emplace(dev, d);
   return d;
 }
 
@@ -902,13 +912,8 @@ const uint8_t *ver_consts(const rs_poly_plan &P) {
   std::vector<uint8_t> h(kEncTablesOff + tab.size(), 0);
   std::memcpy(h.data(), &gp, sizeof(gp));
   std::memcpy(h.data() + kEncTablesOff, tab.data(), tab.size());
-  uint8_t *d = nullptr;
-  if (cudaMalloc(reinterpret_cast<void **>(&d), h.size()) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-    cudaFree(d);
-    return nullptr;
-  }
-  P.ver_dev.emplace(dev, d);
+  uint8_t *d = upload_plan_consts(h);
+  if (d) P.ver_dev.emplace(dev, d);
   return d;
 }
 
@@ -1036,6 +1041,36 @@ rs_status rs_poly_prepare(const rs_poly_plan *P, const int32_t *erasures, size_t
   for (auto &e : wait)
     if (e->fut.valid()) e->fut.wait();
   return RS_OK;
+}
+
+rs_status rs_poly_prepare_all(const rs_poly_plan *P, int max_t, size_t max_patterns) {
+  NvtxRange nvtx_("rs_poly_prepare_all");
+  if (!P || max_t < 0 || max_t > P->m) return RS_ERR_INVALID_ARG;
+  const int n = P->n, m = P->m;
+  uint64_t total = 0;
+  for (int t = 1; t <= max_t; ++t) {  // C(n, t), exact in 64 bits for these sizes
+    uint64_t c = 1;
+    for (int q = 0; q < t; ++q) c = c * (uint64_t)(n - q) / (uint64_t)(q + 1);
+    total += c;
+    if (total > max_patterns || total > kMaxJitKernels) return RS_ERR_INVALID_ARG;
+  }
+  if (total == 0) return RS_OK;
+  std::vector<int32_t> rows;
+  rows.reserve((size_t)total * (size_t)m);
+  std::vector<int> e;
+  for (int t = 1; t <= max_t; ++t) {  // lexicographic t-subsets of [0, n)
+    e.resize(t);
+    for (int q = 0; q < t; ++q) e[q] = q;
+    for (;;) {
+      for (int q = 0; q < m; ++q) rows.push_back(q < t ? e[q] : -1);
+      int q = t - 1;
+      while (q >= 0 && e[q] == n - t + q) --q;
+      if (q < 0) break;
+      ++e[q];
+      for (int r = q + 1; r < t; ++r) e[r] = e[r - 1] + 1;
+    }
+  }
+  return rs_poly_prepare(P, rows.data(), (size_t)total);
 }
 
 size_t rs_poly_jit_source(const rs_poly_plan *P, const int *erasures, int n_erasures, char *buf, size_t cap) {

@@ -425,22 +425,30 @@ cudaError_t launch_generic(int w, const GenericArgs &a, cudaStream_t st) {
   if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
   count_launch();
   const bool verify = a.flags != nullptr;
+  // The dynamic shared-memory opt-in is a per-device (per-context) function attribute:
+  // set it once on every device the kernels launch on.
+  static std::atomic<uint32_t> attr_done[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint32_t bit = w == 8 ? 1u : 2u;
+  if (dev >= 0 && dev < 64 && !(attr_done[dev].load() & bit)) {
+    const int cap = kMaxN * (w == 8 ? 128 : 512);
+    const bool ok = w == 8
+        ? cudaFuncSetAttribute(generic_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap) ==
+                  cudaSuccess &&
+              cudaFuncSetAttribute(generic_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap) ==
+                  cudaSuccess
+        : cudaFuncSetAttribute(generic_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap) ==
+                  cudaSuccess &&
+              cudaFuncSetAttribute(generic_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap) ==
+                  cudaSuccess;
+    if (ok) attr_done[dev].fetch_or(bit);
+    else cudaGetLastError();
+  }
   if (w == 8) {
-    static bool attr8 = (cudaFuncSetAttribute(generic_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              kMaxN * 128) == cudaSuccess) &&
-                        (cudaFuncSetAttribute(generic_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              kMaxN * 128) == cudaSuccess);
-    (void)attr8;
     if (verify) generic_kernel<8, true><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
     else generic_kernel<8, false><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
   } else {
-    static bool attr16 = (cudaFuncSetAttribute(generic_kernel<16, false>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxN * 512) ==
-                          cudaSuccess) &&
-                         (cudaFuncSetAttribute(generic_kernel<16, true>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxN * 512) ==
-                          cudaSuccess);
-    (void)attr16;
     if (verify) generic_kernel<16, true><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
     else generic_kernel<16, false><<<(unsigned)grid, 256, a.smem_bytes, st>>>(a);
   }

@@ -144,7 +144,11 @@ def encode_distributed_p2p(lay: Layout, store: dict, S: int, nbytes: int, rank: 
     """SPMD, fused compute + transfer.  `peer_recv[r]` is rank r's receive buffer ([rows,
     nbytes]; rows >= len(recv_slots(lay, r, S))) as seen from this rank -- a peer-mapped
     view (symmetric memory) on GPUs.  `barrier()` returns once every rank's partial stores
-    are complete and visible.  Same result as encode_distributed."""
+    are complete and visible.  Same result as encode_distributed.
+
+    Reuse contract: the receive buffers may be reused by the next call.  A second barrier
+    after the XOR reduction keeps a fast rank's next partial stores out of a peer's slots
+    until that peer has read them."""
     k, m, N = lay.k, lay.m, lay.world
     like = next(iter(store.values()))
     slots = [recv_slots(lay, d, S) for d in range(N)]
@@ -180,8 +184,31 @@ def encode_distributed_p2p(lay: Layout, store: dict, S: int, nbytes: int, rank: 
     for nsrc, items in by_n.items():
         ops.xor_reduce([store[(s, k + i)] for s, i, _ in items],
                        [[store[(s, k + i)]] + parts for s, i, parts in items], nbytes)
+    barrier()  # every rank has consumed its slots: the buffers may be written again
     return {"sent_blocks": sent, "received_blocks": len(slots[rank]), "local_partial_calls": len(groups),
             "xor_calls": len(by_n)}
+
+
+def check_peer_access(group=None, can_access=None, device=None) -> None:
+    """Raise on every rank (instead of hanging in the rendezvous or faulting in a kernel)
+    unless each rank's GPU can map every other rank's GPU of the group
+    (cudaDeviceCanAccessPeer; NVLink / NVSwitch).  Ranks on the same device need none."""
+    import torch
+    import torch.distributed as dist
+    if can_access is None:
+        can_access = torch.cuda.can_device_access_peer
+    me = torch.cuda.current_device() if device is None else device
+    devs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(devs, me, group=group)
+    missing = sorted({d for d in devs if d != me and not can_access(me, d)})
+    report = [None] * len(devs)
+    dist.all_gather_object(report, (me, missing), group=group)
+    bad = [(d, miss) for d, miss in report if miss]
+    if bad:
+        raise RuntimeError("no CUDA peer access (cudaDeviceCanAccessPeer) for "
+                           + ", ".join(f"cuda:{d} -> cuda:{miss}" for d, miss in bad)
+                           + ": the fused placement needs NVLink peer mappings; use encode_distributed "
+                             "(all_to_all) instead")
 
 
 def symmetric_recv_buffers(lay: Layout, S: int, nbytes: int, group=None):
@@ -190,6 +217,7 @@ def symmetric_recv_buffers(lay: Layout, S: int, nbytes: int, group=None):
     import torch
     import torch.distributed as dist
     import torch.distributed._symmetric_memory as symm_mem
+    check_peer_access(group)
     rows = max(max(len(recv_slots(lay, d, S)) for d in range(lay.world)), 1)
     buf = symm_mem.empty((rows, nbytes), dtype=torch.uint8, device=torch.cuda.current_device())
     hdl = symm_mem.rendezvous(buf, group or dist.group.WORLD)

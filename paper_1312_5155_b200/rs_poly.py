@@ -41,6 +41,7 @@ _lib.rs_poly_plan_set_jit.argtypes = [_vp, _i32]
 _lib.rs_poly_plan_set_read_policy.argtypes = [_vp, _i32]
 _lib.rs_poly_prepare.argtypes = [_vp, _vp, _sz]
 _lib.rs_poly_plan_stats.argtypes = [_vp, _vp]
+_lib.rs_poly_prepare_all.argtypes = [_vp, _i32, _sz]
 _lib.rs_poly_jit_source.argtypes = [_vp, _vp, _i32, ctypes.c_char_p, _sz]
 _lib.rs_poly_jit_source.restype = _sz
 _lib.rs_poly_update.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]
@@ -114,8 +115,33 @@ def _ptr(x) -> int:
     return int(x)
 
 
-def _geometry(stripes, n: int):
+def _where(x, device: bool):
+    """Device entry points take CUDA tensors on the current device; host ones numpy arrays or
+    CPU tensors.  A mismatch would be an illegal address inside a kernel (a sticky context
+    error) or a kernel on another GPU's stream, so it is refused here."""
+    if hasattr(x, "is_cuda"):
+        if device:
+            if not x.is_cuda:
+                raise ValueError("expected a CUDA tensor (this entry point reads device memory)")
+            import torch
+            if x.device.index != torch.cuda.current_device():
+                raise ValueError(f"tensor is on cuda:{x.device.index} but the current device is "
+                                 f"cuda:{torch.cuda.current_device()} (use torch.cuda.device(...))")
+        elif x.is_cuda:
+            raise ValueError("expected host memory (numpy array or CPU tensor), got a CUDA tensor")
+    elif isinstance(x, np.ndarray) and device:
+        raise ValueError("expected a CUDA tensor, got a numpy (host) array")
+
+
+def _dptr(x) -> int:
+    """Address of a device buffer (tensor checked by _where; raw ints are taken as given)."""
+    _where(x, True)
+    return _ptr(x)
+
+
+def _geometry(stripes, n: int, device: bool = True):
     """(ptr, S, stripe_stride, block_stride, block_bytes) of a [S][n][B] uint8 array/tensor."""
+    _where(stripes, device)
     shape = tuple(stripes.shape)
     if len(shape) != 3 or shape[1] != n:
         raise ValueError(f"expected a [S][{n}][B] uint8 array, got shape {shape}")
@@ -129,6 +155,8 @@ def _geometry(stripes, n: int):
         st = stripes.strides
     if st[2] != 1:
         raise ValueError("blocks must be contiguous (last stride 1)")
+    if st[0] < 0 or st[1] < 0:
+        raise ValueError("negative strides are not supported")
     return _ptr(stripes), shape[0], st[0], st[1], shape[2]
 
 
@@ -178,6 +206,12 @@ class Plan:
         er = np.ascontiguousarray(np.asarray(erasures, dtype=np.int32)).reshape(-1, self.m)
         _check(_lib.rs_poly_prepare(self._h, er.ctypes.data, er.shape[0]), "rs_poly_prepare")
 
+    def prepare_all(self, max_t: int | None = None, max_patterns: int = 8192) -> None:
+        """Compile the decode kernel of every pattern of 1..max_t (default m) erasures now
+        (rs_poly_prepare_all): no decode call then waits on, or falls back from, a JIT compile."""
+        t = self.m if max_t is None else max_t
+        _check(_lib.rs_poly_prepare_all(self._h, t, max_patterns), "rs_poly_prepare_all")
+
     def stats(self) -> dict:
         st = Stats()
         _check(_lib.rs_poly_plan_stats(self._h, ctypes.byref(st)), "rs_poly_plan_stats")
@@ -207,12 +241,12 @@ class Plan:
 
     # ---- single stripe -------------------------------------------------------
     def encode(self, data, parity, block_bytes: int, stream=None) -> None:
-        d = (ctypes.c_void_p * self.k)(*[_ptr(x) for x in data])
-        p = (ctypes.c_void_p * self.m)(*[_ptr(x) for x in parity])
+        d = (ctypes.c_void_p * self.k)(*[_dptr(x) for x in data])
+        p = (ctypes.c_void_p * self.m)(*[_dptr(x) for x in parity])
         _check(_lib.rs_poly_encode(self._h, d, p, block_bytes, _stream(stream)), "rs_poly_encode")
 
     def decode(self, blocks, block_bytes: int, erasures, stream=None) -> None:
-        b = (ctypes.c_void_p * self.n)(*[_ptr(x) for x in blocks])
+        b = (ctypes.c_void_p * self.n)(*[_dptr(x) for x in blocks])
         er = list(erasures)
         e = (ctypes.c_int * max(1, len(er)))(*er)
         _check(_lib.rs_poly_decode(self._h, b, block_bytes, e, len(er), _stream(stream)), "rs_poly_decode")
@@ -234,9 +268,9 @@ class Plan:
         idx = list(data_idx)
         c = len(idx)
         ix = (ctypes.c_int * max(1, c))(*idx)
-        o = (ctypes.c_void_p * max(1, c))(*[_ptr(x) for x in old_data])
-        nw = (ctypes.c_void_p * max(1, c))(*[_ptr(x) for x in new_data])
-        p = (ctypes.c_void_p * self.m)(*[_ptr(x) for x in parity])
+        o = (ctypes.c_void_p * max(1, c))(*[_dptr(x) for x in old_data])
+        nw = (ctypes.c_void_p * max(1, c))(*[_dptr(x) for x in new_data])
+        p = (ctypes.c_void_p * self.m)(*[_dptr(x) for x in parity])
         _check(_lib.rs_poly_update(self._h, ix, c, o, nw, p, block_bytes, _stream(stream)), "rs_poly_update")
 
     def update_batch(self, stripes, data_idx, old_blocks, stream=None) -> None:
@@ -248,7 +282,10 @@ class Plan:
         shape = tuple(old_blocks.shape)
         if c and (len(shape) != 3 or shape[0] != S or shape[1] != c or shape[2] != B):
             raise ValueError(f"old_blocks must be [{S}][{c}][{B}]")
+        _where(old_blocks, True)
         ost = old_blocks.stride() if hasattr(old_blocks, "stride") else old_blocks.strides
+        if ost[0] < 0 or ost[1] < 0:
+            raise ValueError("negative strides are not supported")
         _check(_lib.rs_poly_update_batch(self._h, ptr, S, ss, bs, B, ix, c, _ptr(old_blocks), ost[0], ost[1],
                                          _stream(stream)), "rs_poly_update_batch")
 
@@ -275,16 +312,16 @@ class Plan:
         idx = list(data_idx)
         c, S = len(idx), len(partial)
         ix = (ctypes.c_int * max(1, c))(*idx)
-        d = (ctypes.c_void_p * max(1, S * c))(*[_ptr(x) for row in data for x in row])
-        p = (ctypes.c_void_p * (S * self.m))(*[_ptr(x) for row in partial for x in row])
+        d = (ctypes.c_void_p * max(1, S * c))(*[_dptr(x) for row in data for x in row])
+        p = (ctypes.c_void_p * (S * self.m))(*[_dptr(x) for row in partial for x in row])
         _check(_lib.rs_poly_encode_partial(self._h, ix, c, d, p, S, block_bytes, int(accumulate), _stream(stream)),
                "rs_poly_encode_partial")
 
     def xor_reduce(self, dst, srcs, nbytes: int, stream=None) -> None:
         """dst[s] = XOR of srcs[s][*] (lists of pointers/tensors; dst may alias a source)."""
         S, n_src = len(dst), len(srcs[0])
-        dp = (ctypes.c_void_p * S)(*[_ptr(x) for x in dst])
-        sp = (ctypes.c_void_p * (S * n_src))(*[_ptr(x) for row in srcs for x in row])
+        dp = (ctypes.c_void_p * S)(*[_dptr(x) for x in dst])
+        sp = (ctypes.c_void_p * (S * n_src))(*[_dptr(x) for row in srcs for x in row])
         _check(_lib.rs_poly_xor_reduce(self._h, dp, sp, n_src, S, nbytes, _stream(stream)), "rs_poly_xor_reduce")
 
     # ---- the paper's optimisation study (NEXT-3) -----------------------------------
@@ -299,6 +336,7 @@ class Plan:
     def verify_batch(self, stripes, flags, stream=None) -> None:
         """flags[s] = 0 if every column of stripe s is a codeword, else 1 (flags: int32 device [S])."""
         ptr, S, ss, bs, B = _geometry(stripes, self.n)
+        _where(flags, True)
         if tuple(flags.shape) != (S,) or flags.element_size() != 4:
             raise ValueError(f"flags must be a 32-bit device tensor [{S}]")
         _check(_lib.rs_poly_verify_batch(self._h, ptr, S, ss, bs, B, _ptr(flags), _stream(stream)),
@@ -306,14 +344,14 @@ class Plan:
 
     # ---- end to end from host memory --------------------------------------------
     def encode_host(self, host_stripes, stream=None):
-        ptr, S, ss, bs, B = _geometry(host_stripes, self.n)
+        ptr, S, ss, bs, B = _geometry(host_stripes, self.n, device=False)
         h2d, d2h = _u64(), _u64()
         _check(_lib.rs_poly_encode_host(self._h, ptr, S, ss, bs, B, _stream(stream), ctypes.byref(h2d),
                                         ctypes.byref(d2h)), "rs_poly_encode_host")
         return int(h2d.value), int(d2h.value)
 
     def decode_host(self, host_stripes, erasures, stream=None):
-        ptr, S, ss, bs, B = _geometry(host_stripes, self.n)
+        ptr, S, ss, bs, B = _geometry(host_stripes, self.n, device=False)
         er = _erasure_table(erasures, S, self.m)
         h2d, d2h = _u64(), _u64()
         _check(_lib.rs_poly_decode_host(self._h, ptr, S, ss, bs, B, er.ctypes.data, _stream(stream),
@@ -331,6 +369,7 @@ def synth_fill(stripes, k: int, seed: int, stripe0: int = 0, stream=None) -> Non
     if _synth is None:
         _synth = ctypes.CDLL(SYNTH_PATH)
         _synth.rs_synth_fill.argtypes = [_vp, _sz, _sz, _sz, _sz, _i32, _u32, _u32, _vp]
+    _where(stripes, True)
     shape = tuple(stripes.shape)
     ptr, S, ss, bs, B = _ptr(stripes), shape[0], stripes.stride()[0], stripes.stride()[1], shape[2]
     rc = _synth.rs_synth_fill(ptr, S, ss, bs, B, k, seed, stripe0, _stream(stream))

@@ -44,7 +44,7 @@ def declared_functions():
 def test_every_declared_symbol_is_exported(rs):
     libs = {"rs_poly.h": ctypes.CDLL(rs.LIB_PATH), "rs_synth.h": ctypes.CDLL(rs.SYNTH_PATH)}
     decl = declared_functions()
-    assert len(decl) == 27  # 26 in rs_poly.h + rs_synth_fill
+    assert len(decl) == 28  # 27 in rs_poly.h + rs_synth_fill
     for header, name in decl:
         assert hasattr(libs[header], name), f"{name} declared in {header} but not exported"
 
@@ -267,3 +267,22 @@ def test_headers_are_plain_c_and_demo_links():
                             "-lrs_poly", "-lrs_synth", "-L", "/usr/local/cuda/lib64", "-lcudart",
                             "-o", os.path.join(d, "demo")], capture_output=True, text=True)
         assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_prepare_all_enumerates_every_pattern_host_only(rs):
+    """rs_poly_prepare_all: sum_t C(n, t) patterns; bounds checked before anything is built
+    (JIT off here: only the host-side Opt1/Opt3 constants, no GPU needed)."""
+    from math import comb
+    plan = rs.Plan(10, 4, 8, 0x11D)
+    plan.set_jit(rs.RS_JIT_OFF)
+    with pytest.raises(rs.RSError):
+        plan.prepare_all(5)                       # max_t > m
+    with pytest.raises(rs.RSError):
+        plan.prepare_all(4, max_patterns=1469)    # 1470 patterns for RS(10,4)
+    assert plan.stats()["patterns"] == 0          # nothing prepared on a refused call
+    plan.prepare_all(0)
+    plan.prepare_all(2)
+    assert plan.stats()["patterns"] == comb(14, 1) + comb(14, 2)
+    plan.prepare_all()
+    assert plan.stats()["patterns"] == sum(comb(14, t) for t in range(1, 5)) == 1470
+    plan.close()

@@ -17,33 +17,7 @@ import torch.multiprocessing as mp
 import oracle
 import synth
 
-P8 = 0x11D
-
-
-class OracleOps:
-    """CPU stand-ins: partial = oracle encoding of the stripe with only blocks idx non-zero."""
-
-    def __init__(self, k, m):
-        self.k, self.m = k, m
-
-    def encode_partial(self, idx, data, partial, nbytes):
-        for drow, prow in zip(data, partial):
-            st = np.zeros((1, self.k + self.m, nbytes), dtype=np.uint8)
-            for j, d in zip(idx, drow):
-                st[0, j] = d.numpy()
-            oracle.encode_bulk(st, self.k, self.m, 8, P8)
-            for i in range(self.m):
-                prow[i].copy_(torch.from_numpy(st[0, self.k + i].copy()))
-
-    def xor_reduce(self, dst, srcs, nbytes):
-        for d, row in zip(dst, srcs):
-            acc = np.zeros(nbytes, dtype=np.uint8)
-            for x in row:
-                acc ^= x.numpy()
-            d.copy_(torch.from_numpy(acc))
-
-    def empty(self, nblocks, nbytes, like):
-        return torch.empty((nblocks, nbytes), dtype=torch.uint8)
+from tests.placement_ops import P8, OracleOps  # noqa: E402
 
 
 def _worker(rank, world, k, m, S, B, port, q):
@@ -136,3 +110,52 @@ def test_placement_p2p_protocol_gloo(world, k, m):
         p.join(timeout=60)
     assert all(bad == 0 for _, bad, _ in res), res
     assert sum(st["sent_blocks"] for _, _, st in res) == sum(st["received_blocks"] for _, _, st in res)
+
+
+def test_placement_launched_like_bench_gloo():
+    """The SPMD job through bench.py's launcher path (`--gpus 2` re-executes under
+    torch.distributed.run): gloo ranks, oracle compute steps, all_to_all exchange, two calls
+    reusing the buffers, every owned block equal to the oracle's encoding."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    env.pop("WORLD_SIZE", None)
+    p = subprocess.run([sys.executable, os.path.join(root, "tests", "placement_worker.py"), "--gpus", "2",
+                        "--backend", "gloo"], capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["world"] == 2 and d["mismatched_blocks"] == 0 and d["sent_blocks"] == d["received_blocks"] > 0
+
+
+def _worker_peer_check(rank, world, port, allow, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1312_5155_b200.placement import check_peer_access
+    try:
+        check_peer_access(device=rank, can_access=lambda a, b: allow)
+        q.put((rank, "ok"))
+    except RuntimeError as e:
+        q.put((rank, str(e)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("allow", [True, False])
+def test_peer_access_guard_raises_on_every_rank(allow):
+    """Without peer access the fused path refuses on every rank with a clear error (no hang)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29800 + int(allow)
+    ps = [ctx.Process(target=_worker_peer_check, args=(r, 2, port, allow, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    if allow:
+        assert res == {0: "ok", 1: "ok"}
+    else:
+        assert all("peer access" in v and "cuda:0 -> cuda:[1]" in v for v in res.values()), res

@@ -75,6 +75,34 @@ def test_prepare_then_decode_uses_only_jit():
     assert st2["table_launches"] == 0 and st2["jit_launches"] == runs
 
 
+def test_prepare_all_then_any_pattern_runs_jit_only():
+    """rs_poly_prepare_all: every <= m pattern compiled up front; a batch of never-requested
+    random patterns (all of 1..m erasures) then decodes on JIT kernels only, bit-exactly."""
+    from math import comb
+    k, m, B, S = 6, 3, 32 * 1024, 24
+    ref = encoded(k, m, 8, P8, B, S, seed=27)
+    rng = np.random.default_rng(5)
+    er = np.full((S, m), -1, dtype=np.int32)
+    for s in range(S):
+        t = 1 + s % m
+        er[s, :t] = rng.choice(k + m, t, replace=False)
+    m_ = rs()
+    plan = m_.Plan(k, m)
+    plan.prepare_all()
+    st = plan.stats()
+    n_pat = sum(comb(k + m, t) for t in range(1, m + 1))
+    assert st["patterns"] == n_pat and st["jit_ready"] == n_pat and st["jit_pending"] == 0
+    bad = ref.copy()
+    for s in range(S):
+        bad[s, er[s][er[s] >= 0]] = 0x77
+    d = torch.from_numpy(bad).cuda()
+    plan.decode_batch(d, er)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    st2 = plan.stats()
+    assert st2["table_launches"] == 0 and st2["jit_launches"] > 0
+
+
 def test_background_mode_converges():
     """Background JIT: first calls use tables, later ones the compiled kernels; always exact."""
     import time

@@ -3,7 +3,9 @@
 behind a ~10 ms GPU sleep (the host is then ahead of the GPU): the difference is host work
 before the GPU can start (RS_POLY_HOST_PROFILE=1 prints the phases on stderr).  Prints % of
 the MEASURED_PEAKS copy figure and the host time of each call (h, ms).
-usage: python tools/start_latency.py [C3|C4|C5 ...]"""
+usage: python tools/start_latency.py [C3|C4|C5 ...]
+       python tools/start_latency.py cold [C5|C4 ...]   # first decode of a fresh plan:
+         background JIT (new patterns on the table kernels) vs after rs_poly_prepare_all"""
 import os
 import sys
 import time
@@ -51,6 +53,48 @@ def run(cfg):
     torch.cuda.empty_cache()
 
 
+def cold(cfg):
+    """First decode call of a fresh plan (patterns never seen) vs its warm figure: without
+    preparation (background JIT: the new patterns run on the table kernels) and after
+    rs_poly_prepare_all (every <= m pattern compiled up front; time reported)."""
+    c = synth.CONFIGS[cfg]
+    k, m, w, B, S = c["k"], c["m"], c["w"], c["block_bytes"], c["stripes"]
+    st = torch.empty((S, k + m, B), dtype=torch.uint8, device="cuda")
+    rsp.synth_fill(st, k, seed=0)
+    er = synth.erasure_table(cfg, 0, S)
+    moved = S * (k + m) * B
+
+    def call(plan):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        plan.decode_batch(st, er)
+        e1.record()
+        torch.cuda.synchronize()
+        return moved / e0.elapsed_time(e1) / 1e6 / PEAK
+
+    for mode in ("no preparation", "prepare_all"):
+        plan = rsp.Plan(k, m, w, c["poly"])
+        t0 = time.perf_counter()
+        if mode == "prepare_all":
+            plan.prepare_all()
+        setup = time.perf_counter() - t0
+        first = call(plan)
+        plan.prepare(er)
+        warm = sorted(call(plan) for _ in range(5))[2]
+        stt = plan.stats()
+        print(f"{cfg} cold decode, {mode}: first {first:.3f} warm {warm:.3f} ratio {first / warm:.3f} "
+              f"setup {setup:.1f} s patterns {stt['patterns']} jit_ready {stt['jit_ready']} "
+              f"cache_hits {stt['jit_cache_hits']}", flush=True)
+        plan.close()
+    del st
+    torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
-    for cfg in sys.argv[1:] or ["C4", "C3", "C5"]:
-        run(cfg)
+    if sys.argv[1:2] == ["cold"]:
+        for cfg in sys.argv[2:] or ["C5"]:
+            cold(cfg)
+    else:
+        for cfg in sys.argv[1:] or ["C4", "C3", "C5"]:
+            run(cfg)
