@@ -108,16 +108,16 @@ def code_hash() -> str:
 
 
 def ncu_traffic(cfg: str, op: str):
-    """(DRAM bytes per call, source note) of one whole call from the committed ncu capture
-    (tools/ncu_traffic.py); (None, why) unless it was taken on this exact library source."""
+    """(DRAM bytes per call, ncu DRAM GB/s, source note) of one whole call from the committed ncu
+    capture (tools/ncu_traffic.py); (None, None, why) unless taken on this exact library source."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             e = json.load(f)[cfg][op]
     except Exception:
-        return None, "no capture for this config"
+        return None, None, "no capture for this config"
     if e.get("code_hash") != code_hash():
-        return None, f"capture is of code {e.get('code_hash')}, not this build ({code_hash()}): refused"
-    return int(e["bytes_per_call"]), e.get("source", "")
+        return None, None, f"capture is of code {e.get('code_hash')}, not this build ({code_hash()}): refused"
+    return int(e["bytes_per_call"]), e.get("ncu_dram_gbs"), e.get("source", "")
 
 
 def allreduce(x: float, op: str, world: int, device) -> float:
@@ -445,7 +445,7 @@ def run_ours(args):
     dec_kernel = "rs_jit (per-pattern NVRTC XOR network)" if jst["jit_launches"] else "sliced_kernel decode (tables)"
     dom_ms, dom_name = (dec_avg, "decode: " + dec_kernel) if dec_avg >= enc_avg else (enc_avg, "encode: sliced_kernel")
     achieved = moved / (dom_ms / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic(args.config, "decode" if dom_name.startswith("decode") else "encode")
+    traffic, ncu_gbs, traffic_src = ncu_traffic(args.config, "decode" if dom_name.startswith("decode") else "encode")
 
     # ---- end to end through the public API from pinned host memory ----
     e2e = None
@@ -483,6 +483,8 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                      "traffic_over_algorithmic": round(traffic / moved, 4) if traffic else None,
+                     "ncu_dram_gbs": ncu_gbs,
+                     "dram_gbs_in_run": round(traffic / (dom_ms / 1e3) / 1e9, 1) if traffic else None,
                      "code_hash": code_hash(),
                      "kernel": f"{dom_name}; {moved} algorithmic bytes per call = S*(k+m)*B, avg {dom_ms:.4f} ms",
                      "peak_source": peak_src,
