@@ -148,32 +148,18 @@ rsb::jit::Spec jit_spec(const rs_poly_plan &P, const std::vector<int> &in, const
   // (RS(10,4) decode: 36 B spilled at 128 registers, grouping costs more than it saves);
   // beyond that it spills 136-300 B per thread, and groups of 10 - outputs blocks spill
   // nothing for +6-14% LOP3 (r01q: RS(10,6) encode 93% -> 103%, decode 77% -> 92%).
-  static const int w8_group = [] {  // RS_POLY_JIT_W8_GROUP overrides (measurement knob)
-    const char *e = std::getenv("RS_POLY_JIT_W8_GROUP");
-    return e ? (int)std::max(0L, std::min(std::strtol(e, nullptr, 10), 64L)) : -1;
-  }();
   const int n_io = (int)(in.size() + out.size());
-  const int w8_auto = n_io > 14 ? std::max(2, 10 - (int)out.size()) : 0;
-  s.group_blocks = P.w == 8 ? (w8_group >= 0 ? w8_group : w8_auto) : 3;
+  s.group_blocks = P.w == 8 ? (n_io > 14 ? std::max(2, 10 - (int)out.size()) : 0) : 3;
   // w8 at 4 CTAs/SM (128 registers): 3 CTAs/SM without spills is slower even for 5-6
-  // outputs (r01q: RS(10,5) encode 88% vs 105%).
-  static const int w8_minb = [] {  // RS_POLY_JIT_W8_MINB (measurement knob, default 4)
-    const char *e = std::getenv("RS_POLY_JIT_W8_MINB");
-    return e ? (int)std::max(1L, std::min(std::strtol(e, nullptr, 10), 8L)) : 4;
-  }();
-  s.min_blocks = P.w == 8 ? w8_minb : 3;
+  // outputs (r01q: RS(10,5) encode 88% vs 105%; 5 CTAs/SM spills more, profiles/r01q_w8_jit_occupancy.log).
+  s.min_blocks = P.w == 8 ? 4 : 3;
   return s;
 }
 
-// __launch_bounds__ min CTAs/SM of the w16 JIT kernels (RS_POLY_JIT_W16_MINB, default 3:
-// 168 registers, no spill; 4 caps them at 128 and spills ~400 B).
-int jit_w16_min_blocks() {
-  static const int v = [] {
-    const char *e = std::getenv("RS_POLY_JIT_W16_MINB");
-    return e ? (int)std::max(1L, std::min(std::strtol(e, nullptr, 10), 8L)) : 3;
-  }();
-  return v;
-}
+// __launch_bounds__ min CTAs/SM of the w16 JIT kernels: 3 (168 registers); 4 caps them at
+// 128 and spills ~400 B (r01: 68% vs 80%), 2 (225 registers, no spill) is slower too
+// (r02c: C4 per-stripe decode 0.76 vs 0.86 of the copy peak, profiles/r02c_w16_occupancy.log).
+constexpr int kJitW16MinBlocks = 3;
 
 // The encoder kernel of a code without a compiled network: w = 8 the parity-map
 // network, w = 16 the syndrome form (Horner over the data, then Q).
@@ -188,7 +174,7 @@ rsb::jit::Spec encoder_spec(const rs_poly_plan &P) {
     s.T = P.m;
     s.M = rsb::horner_q(P.F, P.m);
     for (int j = P.k - 1; j >= 0; --j) s.seq.push_back(j);  // positions m+k-1 .. m
-    s.min_blocks = jit_w16_min_blocks();
+    s.min_blocks = kJitW16MinBlocks;
   }
   return s;
 }
@@ -208,7 +194,7 @@ rsb::jit::Spec decoder_spec(const rs_poly_plan &P, const PatternHost &ph) {
       const int b = pos >= P.m ? pos - P.m : P.k + pos;  // inverse of rsb::position
       s.seq.push_back(er[b] ? -1 : b);
     }
-    s.min_blocks = jit_w16_min_blocks();
+    s.min_blocks = kJitW16MinBlocks;
   }
   return s;
 }
@@ -270,14 +256,11 @@ std::vector<cudaStream_t> side_streams(const rs_poly_plan &P) {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(P.mu);
   auto &v = P.pool[dev];
-  // Extra PDL chains for the per-pattern JIT launches.  Default: one extra for w = 8 (two
-  // ~20 KB kernels share an SM well: C3 decode 89% -> 96%), none for w = 16 (two ~60 KB
-  // kernels thrash the instruction cache: C4 78% -> 56%).  RS_POLY_SIDE_STREAMS overrides.
-  static const long env = [] {
-    const char *e = std::getenv("RS_POLY_SIDE_STREAMS");
-    return e ? std::max(0L, std::min(std::strtol(e, nullptr, 10), 63L)) : -1L;
-  }();
-  const size_t want = env >= 0 ? (size_t)env : (P.w == 8 ? 1 : 0);
+  // Extra PDL chains for the per-pattern JIT launches: one extra for w = 8 (two ~20 KB
+  // kernels share an SM well: C3 decode 89% -> 96%), none for w = 16 (two ~60 KB kernels
+  // thrash the instruction cache: C4 78% -> 56%; profiles/r01q_side_streams.log,
+  // r01t_w16_side_stream_recheck.log).
+  const size_t want = P.w == 8 ? 1 : 0;
   if (want == 0) return {};
   while (v.size() < want) {
     cudaStream_t s = nullptr;
@@ -305,17 +288,13 @@ int sm_count() {
   return v;
 }
 
-// Units (32 columns each) per CTA so that a launch has about RS_POLY_CTAS_PER_SM CTAs per SM (default 4 for
-// w = 8, 8 for w = 16), in multiples of the CTA size, at most kSlicedUnitsPerCta.  Measured
+// Units (32 columns each) per CTA so that a launch has about 4 (w = 8) or 8 (w = 16) CTAs
+// per SM, in multiples of the CTA size, at most kSlicedUnitsPerCta.  Measured
 // on per-stripe decode chains (r01p): w = 8 (C3, 4 CTAs/SM resident) runs best with 2 units
 // per thread (97% vs 94% of the copy peak with 1, 92% with 4); w = 16 (3 CTAs/SM, a 4x
 // longer body per unit) with 1 (80% vs 68% with 2).
 uint32_t units_per_cta_for(uint64_t total, int w) {
-  static const long env = [] {
-    const char *e = std::getenv("RS_POLY_CTAS_PER_SM");
-    return e ? std::max(1L, std::min(std::strtol(e, nullptr, 10), 64L)) : 0L;
-  }();
-  const uint64_t per_sm = env ? (uint64_t)env : (w == 8 ? 4 : 8);
+  const uint64_t per_sm = w == 8 ? 4 : 8;
   const uint64_t target = (uint64_t)sm_count() * per_sm;
   uint64_t upc = (total + target - 1) / target;
   upc = (upc + kSlicedThreads - 1) / kSlicedThreads * kSlicedThreads;
@@ -342,11 +321,7 @@ cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32
   if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
   void *args[] = {&a};
   rsb::count_launch();
-  static const bool pdl_on = [] {  // RS_POLY_PDL=0 turns the chaining off (measurement knob)
-    const char *e = std::getenv("RS_POLY_PDL");
-    return !(e && e[0] == '0');
-  }();
-  if (!pdl || !pdl_on)
+  if (!pdl)
     return cudaLaunchKernel(reinterpret_cast<const void *>(k.fn), dim3((unsigned)grid), dim3(kSlicedThreads), args,
                             0, st);
   // programmatic dependent launch (the generated kernels trigger at entry; their last CTA waits at exit)
@@ -738,11 +713,6 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
   // A pattern that recurs on non-adjacent stripes: one lean launch per run of adjacent
   // stripes instead of a stripe list in an uploaded blob (each CTA would first load its
   // stripe index from it -- a dependent global load before any of its data loads).
-  // RS_POLY_SPLIT_RUNS=0 keeps the blob path (measurement knob).
-  static const bool split_runs = [] {
-    const char *e = std::getenv("RS_POLY_SPLIT_RUNS");
-    return !(e && e[0] == '0');
-  }();
   // Only while that adds few launches: at most twice the patterns' (alternating patterns
   // over many small stripes would otherwise turn one launch per pattern into one per stripe).
   size_t n_runs = 0, n_groups = 0;
@@ -750,7 +720,7 @@ rs_status decode_impl(const rs_poly_plan *P, Geometry G, const uint64_t *ptrs,
     n_groups += !gr.empty();
     for (size_t q = 0; q < gr.size(); ++q) n_runs += q == 0 || gr[q] != gr[q - 1] + 1;
   }
-  if (split_runs && any_jit && !any_rt && !ptrs && body * UB == G.block_bytes && n_runs <= 2 * n_groups) {
+  if (any_jit && !any_rt && !ptrs && body * UB == G.block_bytes && n_runs <= 2 * n_groups) {
     std::vector<const rsb::jit::Kernel *> jr;
     std::vector<std::vector<int32_t>> runs;
     jr.reserve(n_runs);
@@ -887,7 +857,7 @@ rsb::jit::Spec verify_spec(const rs_poly_plan &P) {
     s.poly = P.poly;
     s.T = m;
     for (int pos = n - 1; pos >= 0; --pos) s.seq.push_back(pos >= m ? pos - m : P.k + pos);
-    s.min_blocks = jit_w16_min_blocks();
+    s.min_blocks = kJitW16MinBlocks;
   } else {
     s.group_blocks = 10;  // n * 8 input planes in CSE groups of 10 blocks
   }

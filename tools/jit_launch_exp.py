@@ -43,7 +43,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        print(f"{cfg} side_streams={os.environ.get('RS_POLY_SIDE_STREAMS', '3')} {name:10s} "
+        print(f"{cfg} {name:10s} "
               f"patterns={len({tuple(r) for r in er.tolist()})} {ms:.3f} ms  {moved / ms / 1e6:.0f} GB/s moved")
 
 

@@ -54,11 +54,13 @@ def run(cfg: str, op: str) -> None:
     flush.sum()  # warm: the reduction's scratch comes from the caching allocator afterwards
     torch.cuda.synchronize()
     call = (lambda: plan.encode_batch(st)) if op == "encode" else (lambda: plan.decode_batch(st, er))
-    for with_call in (True, False):
+    # ranges 1-2 as documented; 3 (empty) and 4 (two flushes) are diagnostics of the method
+    for calls, flushes in ((1, 1), (0, 1), (0, 0), (0, 2)):
         torch.cuda.profiler.start()
-        if with_call:
+        for _ in range(calls):
             call()
-        flush.sum()  # reads 2 x L2: evicts (writes back) what the call left dirty
+        for _ in range(flushes):
+            flush.sum()  # reads 2 x L2: evicts (writes back) what the call left dirty
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
     print(json.dumps({"cfg": cfg, "op": op, "algorithmic_bytes": S * n * B, "flush_bytes": flush.numel() * 4,
@@ -118,8 +120,10 @@ def summarize(paths: list[str]) -> None:
         }
         lines.append(f"{cfg} {op}: read {rd / 1e9:.4f} GB write {wr / 1e9:.4f} GB total {tot / 1e9:.4f} GB "
                      f"= {tot / alg:.4f} x algorithmic {alg / 1e9:.4f} GB; ncu range {dur * 1e3:.3f} ms "
-                     f"-> {tot / dur / 1e9 if dur > 0 else 0:.1f} GB/s; flush-only range read "
-                     f"{b['dram__bytes_read.sum'] / 1e9:.4f} GB write {b['dram__bytes_write.sum'] / 1e9:.4f} GB")
+                     f"-> {tot / dur / 1e9 if dur > 0 else 0:.1f} GB/s")
+        for i, r in enumerate(rng):
+            lines.append(f"    range {i + 1}: read {r['dram__bytes_read.sum'] / 1e9:.4f} GB write "
+                         f"{r['dram__bytes_write.sum'] / 1e9:.4f} GB time {r['gpu__time_duration.sum'] * 1e3:.3f} ms")
     with open(dst, "w") as f:
         json.dump(db, f, indent=1)
     print("\n".join(lines))
