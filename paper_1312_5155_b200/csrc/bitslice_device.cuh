@@ -178,23 +178,44 @@ __device__ __forceinline__ void horner_step(uint32_t *s, const uint32_t *c) {
   }
 }
 
+// A unit is 32 columns: 32 bytes of a block (w = 8) or 64 (w = 16, two 32-byte halves).  The
+// w = 16 halves are `h2` bytes apart: 32 (contiguous) or, for a full warp, 1024 -- lane l then
+// owns bytes [32 l, 32 l + 32) and [1024 + 32 l, ...) of the warp's 2 KiB, so that each 256-bit
+// load / store instruction of the warp covers 1 KiB contiguously (whole 128-byte lines) instead
+// of every other 32-byte sector of 2 KiB (unit_offset() below).
 template <int W>
-__device__ __forceinline__ void load_unit(const uint8_t *p, uint32_t *x) {
+__device__ __forceinline__ void load_unit(const uint8_t *p, uint32_t *x, uint32_t h2 = 32) {
   ldg_v8(p, x);
-  if (W == 16) ldg_v8(p + 32, x + 8);
+  if (W == 16) ldg_v8(p + h2, x + 8);
 }
 // y ^= the raw bytes of a unit (an input added unchanged to one output, after transpose back)
 template <int W>
-__device__ __forceinline__ void xor_unit(uint32_t *y, const uint8_t *p) {
+__device__ __forceinline__ void xor_unit(uint32_t *y, const uint8_t *p, uint32_t h2 = 32) {
   uint32_t r[W];
-  load_unit<W>(p, r);
+  load_unit<W>(p, r, h2);
 #pragma unroll
   for (int q = 0; q < W; ++q) y[q] ^= r[q];
 }
 template <int W>
-__device__ __forceinline__ void store_unit(uint8_t *p, const uint32_t *x) {
+__device__ __forceinline__ void store_unit(uint8_t *p, const uint32_t *x, uint32_t h2 = 32) {
   stg_v8(p, x);
-  if (W == 16) stg_v8(p + 32, x + 8);
+  if (W == 16) stg_v8(p + h2, x + 8);
+}
+// Byte offset of unit u in its block and the distance h2 of its second half (w = 16).  Units
+// of a warp are consecutive and start at a multiple of 32 (CTA ranges are multiples of 128);
+// a warp whose 32 units all lie below u_end uses the 1 KiB-interleaved halves, a partial one
+// (the end of a stripe) the contiguous layout.  Every block of a stripe uses the same map,
+// so column c's symbols still sit at the same offset in each block.
+template <int W>
+__device__ __forceinline__ uint64_t unit_offset(uint64_t u, uint64_t u_end, uint32_t &h2) {
+  if (W != 16) {
+    h2 = 32;
+    return u * 32ull;
+  }
+  const uint64_t lane = u & 31ull;
+  const bool full = (u - lane) + 32ull <= u_end;
+  h2 = full ? 1024u : 32u;
+  return full ? u * 64ull - lane * 32ull : u * 64ull;
 }
 
 }  // namespace rsb

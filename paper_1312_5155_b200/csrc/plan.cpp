@@ -114,7 +114,16 @@ std::shared_ptr<const PatternHost> build_pattern(const rs_poly_plan &P, const st
     for (int b : er) ph->sp.erased_mask[b >> 5] |= 1u << (b & 31);
     ph->sp.t = t;
     for (int e = 0; e < t && e < 4; ++e) ph->sp.out_blk[e] = (uint8_t)er[e];
-    pack_generic_tables(F, P.w, W, t, m, ph->wtab);  // one group (t <= 4): [i][h][v]
+    if (P.w == 16) {
+      // the w16 table kernel solves from the m syndromes of the received word (design C):
+      // y = [V_E^{-1} | 0] S, S_j for j < m (only j < t enter)
+      std::vector<uint32_t> Vx((size_t)t * m, 0);
+      for (int e = 0; e < t; ++e)
+        for (int j = 0; j < t; ++j) Vx[(size_t)e * m + j] = V[(size_t)e * t + j];
+      pack_generic_tables(F, P.w, Vx, t, m, ph->wtab);
+    } else {
+      pack_generic_tables(F, P.w, W, t, m, ph->wtab);  // one group (t <= 4): [i][h][v]
+    }
   }
   // generic record
   std::memset(&ph->gp, 0, sizeof(ph->gp));
@@ -199,6 +208,40 @@ rsb::jit::Spec decoder_spec(const rs_poly_plan &P, const PatternHost &ph) {
   return s;
 }
 
+// One empty launch (a single CTA with no stripe selected: it returns at once) of a freshly
+// loaded JIT kernel, on a library-private non-blocking stream: the driver's first-launch setup
+// of the function then happens here, at prepare time, not inside the first decode call that
+// uses it (C5 first decode after rs_poly_prepare_all: profiles/r02e_cold.log).  Not counted
+// in rs_poly_launch_count (no user work); errors are dropped.
+void warm_launch(const rsb::jit::Kernel &k) {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaStream_t st = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = streams.find(dev);
+    if (it == streams.end()) {
+      if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+      }
+      streams.emplace(dev, st);
+    } else {
+      st = it->second;
+    }
+  }
+  rsb::jit::Args a{};
+  a.n_sel = 0;
+  a.units_per_cta = kSlicedThreads;
+  a.ctas_per_stripe = 1;
+  void *args[] = {&a};
+  if (cudaLaunchKernel(reinterpret_cast<const void *>(k.fn), dim3(1), dim3(kSlicedThreads), args, 0, st) !=
+      cudaSuccess)
+    cudaGetLastError();
+}
+
 // The compiled kernel for `key` if it is ready; schedules (background) or runs (sync /
 // wait) its compilation on first request.  Must be called without holding P.mu.
 const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const JitKey &key, const std::function<rsb::jit::Spec()> &mk,
@@ -237,6 +280,7 @@ const rsb::jit::Kernel *jit_get(const rs_poly_plan &P, const JitKey &key, const 
       auto k = std::make_shared<rsb::jit::Kernel>(rsb::jit::compile(src));
       k->xors = xors;
       k->w = spec.w;
+      if (k->ok) warm_launch(*k);
       if (!k->ok) {  // loud, once per process (the pattern then runs on the table kernel)
         static std::atomic<int> reported{0};
         if (reported.fetch_add(1) == 0 || std::getenv("RS_POLY_JIT_LOG"))

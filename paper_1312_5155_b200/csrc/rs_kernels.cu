@@ -45,7 +45,7 @@ void count_launch() { g_launches.fetch_add(1); }
 // (group 0 assigns y, later groups accumulate).  Erased data blocks (decode)
 // are not read: their planes are zero.
 template <int K, int M, int W, uint32_t POLY, bool DECODE, int G>
-__device__ __forceinline__ void net_groups(uint8_t *const *blk, uint64_t off, uint32_t emask,
+__device__ __forceinline__ void net_groups(uint8_t *const *blk, uint64_t off, uint32_t h2, uint32_t emask,
                                            uint32_t (&y)[M * W]) {
   using Grp = RsNetGroup<K, M, W, POLY, G>;
   constexpr int J0 = Grp::kFirstBlock, NB = Grp::kBlocks;
@@ -56,14 +56,14 @@ __device__ __forceinline__ void net_groups(uint8_t *const *blk, uint64_t off, ui
 #pragma unroll
       for (int q = 0; q < W; ++q) x[j * W + q] = 0;
     } else {
-      load_unit<W>(blk[J0 + j] + off, &x[j * W]);
+      load_unit<W>(blk[J0 + j] + off, &x[j * W], h2);
     }
   }
 #pragma unroll
   for (int j = 0; j < NB; ++j) transposeW<W>(&x[j * W]);
   Grp::run(x, y);
   if constexpr (G + 1 < RsNet<K, M, W, POLY>::kGroups)
-    net_groups<K, M, W, POLY, DECODE, G + 1>(blk, off, emask, y);
+    net_groups<K, M, W, POLY, DECODE, G + 1>(blk, off, h2, emask, y);
 }
 
 // Syndrome-form encoder (w = 16 instances, RsQNet): H_j = Horner over the data
@@ -80,7 +80,7 @@ __device__ __forceinline__ void horner_all(uint32_t (&h)[M * W], const uint32_t 
 constexpr int kHornerUnroll = RS_W16_HUNROLL > 0 ? RS_W16_HUNROLL : 1;
 
 template <int K, int M, int W, uint32_t POLY, bool DECODE>
-__device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off, uint32_t emask,
+__device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off, uint32_t h2, uint32_t emask,
                                               uint32_t (&y)[M * W]) {
   uint32_t h[M * W];
   {
@@ -89,7 +89,7 @@ __device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off,
 #pragma unroll
       for (int q = 0; q < W; ++q) c[q] = 0;
     } else {
-      load_unit<W>(blk[K - 1] + off, c);
+      load_unit<W>(blk[K - 1] + off, c, h2);
       transposeW<W>(c);
     }
 #pragma unroll
@@ -106,7 +106,7 @@ __device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off,
 #pragma unroll
       for (int q = 0; q < W; ++q) c[q] = 0;
     } else {
-      load_unit<W>(blk[jb] + off, c);
+      load_unit<W>(blk[jb] + off, c, h2);
       transposeW<W>(c);
     }
     horner_all<K, M, W, POLY, DECODE, 0>(h, c);
@@ -114,11 +114,45 @@ __device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off,
   RsQNet<K, M, W, POLY>::run(h, y);
 }
 
+// Syndromes of the received word (w = 16 table decode, SURVEY App. B design C): S_j =
+// sum_p c_p alpha^{j p} over ALL n positions, Horner from the top (x^{n-1} = data K-1) down
+// to x^0 (parity 0) with step alpha^j (Step 1); erased positions (CTA-uniform
+// bits of emask) are not read and enter as zero.  j < M.
+template <int K, int M, int W, uint32_t POLY>
+__device__ __forceinline__ void horner_syndromes(uint8_t *const *blk, uint64_t off, uint32_t h2, uint32_t emask,
+                                                 uint32_t (&h)[M * W]) {
+  {
+    uint32_t c[W];
+    if ((emask >> (K - 1)) & 1u) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) c[q] = 0;
+    } else {
+      load_unit<W>(blk[K - 1] + off, c, h2);
+      transposeW<W>(c);
+    }
+#pragma unroll
+    for (int i = 0; i < M * W; ++i) h[i] = c[i % W];
+  }
+#pragma unroll kHornerUnroll
+  for (int p = K + M - 2; p >= 0; --p) {  // position p: data p - M (p >= M), else parity p
+    const int b = p >= M ? p - M : K + p;
+    uint32_t c[W];
+    if ((emask >> b) & 1u) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) c[q] = 0;
+    } else {
+      load_unit<W>(blk[b] + off, c, h2);
+      transposeW<W>(c);
+    }
+    horner_all<K, M, W, POLY, true, 0>(h, c);
+  }
+}
+
 template <int K, int M, int W, uint32_t POLY, bool DECODE>
-__device__ __forceinline__ void encode_planes(uint8_t *const *blk, uint64_t off, uint32_t emask,
+__device__ __forceinline__ void encode_planes(uint8_t *const *blk, uint64_t off, uint32_t h2, uint32_t emask,
                                               uint32_t (&y)[M * W]) {
-  if constexpr (RsQNet<K, M, W, POLY>::kHorner) horner_encode<K, M, W, POLY, DECODE>(blk, off, emask, y);
-  else net_groups<K, M, W, POLY, DECODE, 0>(blk, off, emask, y);
+  if constexpr (RsQNet<K, M, W, POLY>::kHorner) horner_encode<K, M, W, POLY, DECODE>(blk, off, h2, emask, y);
+  else net_groups<K, M, W, POLY, DECODE, 0>(blk, off, h2, emask, y);
 }
 
 // ---------------------------------------------------------------------------
@@ -136,7 +170,6 @@ constexpr int sliced_min_blocks() { return W == 8 ? 4 : RS_W16_MINB; }
 
 template <int K, int M, int W, uint32_t POLY, bool DECODE>
 __global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(const SlicedArgs a) {
-  constexpr int UB = 32 * W / 8;                    // bytes per unit per block
   constexpr int TAB_WORDS = M * (W / 4) * 16 * (W / 8);  // W-step tables, 32-bit words
   __shared__ __align__(16) uint32_t wtab[DECODE ? TAB_WORDS : 1];
 
@@ -167,26 +200,32 @@ __global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(con
   const uint64_t u0 = (uint64_t)c * a.units_per_cta;
   const uint64_t u1 = min(u0 + a.units_per_cta, a.units_per_stripe);
   for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-    const uint64_t off = u * UB;
+    uint32_t h2;
+    const uint64_t off = unit_offset<W>(u, u1, h2);
     uint32_t y[M * W];
-    encode_planes<K, M, W, POLY, DECODE>(blk, off, emask, y);
+    // w = 16 decode: the m syndromes of the received word (design C); otherwise the encoder
+    constexpr bool kSyn = DECODE && RsQNet<K, M, W, POLY>::kHorner;
+    if constexpr (kSyn) horner_syndromes<K, M, W, POLY>(blk, off, h2, emask, y);
+    else encode_planes<K, M, W, POLY, DECODE>(blk, off, h2, emask, y);
 #pragma unroll
     for (int i = 0; i < M; ++i) transposeW<W>(&y[i * W]);
 
     if (!DECODE) {
 #pragma unroll
-      for (int i = 0; i < M; ++i) store_unit<W>(blk[K + i] + off, &y[i * W]);
+      for (int i = 0; i < M; ++i) store_unit<W>(blk[K + i] + off, &y[i * W], h2);
       continue;
     }
 
-    // Delta_i = received parity_i ^ encode(surviving data)_i (erased parity: received = 0)
+    if constexpr (!kSyn) {
+      // Delta_i = received parity_i ^ encode(surviving data)_i (erased parity: received = 0)
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-      if (!((emask >> (K + i)) & 1u)) {
-        uint32_t r[W];
-        load_unit<W>(blk[K + i] + off, r);
+      for (int i = 0; i < M; ++i) {
+        if (!((emask >> (K + i)) & 1u)) {
+          uint32_t r[W];
+          load_unit<W>(blk[K + i] + off, r, h2);
 #pragma unroll
-        for (int q = 0; q < W; ++q) y[i * W + q] ^= r[q];
+          for (int q = 0; q < W; ++q) y[i * W + q] ^= r[q];
+        }
       }
     }
 
@@ -227,7 +266,7 @@ __global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(con
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (e < t) store_unit<W>(a.L.block(s, outb[e]) + off, o[e]);
+        if (e < t) store_unit<W>(a.L.block(s, outb[e]) + off, o[e], h2);
     } else {
       // w = 16: entries are 4 x 16-bit lanes (uint2), four nibbles per symbol.
       uint2 acc[32];
@@ -264,7 +303,7 @@ __global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(con
             const uint32_t a1 = (e < 2) ? acc[2 * q + 1].x : acc[2 * q + 1].y;
             o[q] = __byte_perm(a0, a1, (e & 1) ? 0x7632 : 0x5410);
           }
-          store_unit<W>(a.L.block(s, outb[e]) + off, o);
+          store_unit<W>(a.L.block(s, outb[e]) + off, o, h2);
         }
       }
     }

@@ -28,16 +28,16 @@ def rs():
 def parse(src):
     ins = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bi(\d+) = blkp\(a, s, (\d+)\);", src)}
     outs = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bo(\d+) = blkp\(a, s, (\d+)\);", src)}
-    w = int(re.search(r"const uint64_t off = u \* (\d+)ull;", src).group(1)) * 8 // 32
+    w = int(re.search(r"const uint64_t off = unit_offset<(\d+)>\(u, u1, h2\);", src).group(1))
     groups = []
     for body in re.findall(r"^    \{\n(.*?)\n    \}$", src, re.S | re.M):
-        loads = [(int(i), int(base)) for i, base in re.findall(r"load_unit<\d+>\(bi(\d+) \+ off, &x\[(\d+)\]\);", body)]
+        loads = [(int(i), int(base)) for i, base in re.findall(r"load_unit<\d+>\(bi(\d+) \+ off, &x\[(\d+)\], h2\);", body)]
         stmts = re.findall(r"^\s+(const uint32_t (t\d+)|y\[(\d+)\]) (\^?=) (.*);$", body, re.M)
         groups.append((loads, stmts))
-    stores = [(int(i), int(base)) for i, base in re.findall(r"store_unit<\d+>\(bo(\d+) \+ off, &y\[(\d+)\]\);", src)]
+    stores = [(int(i), int(base)) for i, base in re.findall(r"store_unit<\d+>\(bo(\d+) \+ off, &y\[(\d+)\], h2\);", src)]
     # pass-through inputs: bytes XORed into an output after its transpose back
     pins = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bp(\d+) = blkp\(a, s, (\d+)\);", src)}
-    passes = [(int(base), pins[int(i)]) for base, i in re.findall(r"xor_unit<\d+>\(&y\[(\d+)\], bp(\d+) \+ off\);", src)]
+    passes = [(int(base), pins[int(i)]) for base, i in re.findall(r"xor_unit<\d+>\(&y\[(\d+)\], bp(\d+) \+ off, h2\);", src)]
     return w, ins, outs, groups, stores, passes
 
 
@@ -48,8 +48,8 @@ def evaluate_horner(src, cw_cols):
     with the oracle by the caller, so a wrong multiply, order or network fails."""
     ins = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bi(\d+) = blkp\(a, s, (\d+)\);", src)}
     outs = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bo(\d+) = blkp\(a, s, (\d+)\);", src)}
-    w = int(re.search(r"const uint64_t off = u \* (\d+)ull;", src).group(1)) * 8 // 32
-    body = src[src.index("const uint64_t off = u *"):]
+    w = int(re.search(r"const uint64_t off = unit_offset<(\d+)>\(u, u1, h2\);", src).group(1))
+    body = src[src.index("const uint64_t off = unit_offset<"):]
     C = cw_cols.shape[1]
     S, x, y, env, res = {}, {}, {}, {}, {}
 
@@ -65,12 +65,12 @@ def evaluate_horner(src, cw_cols):
 
     out_lines = [ln.strip() for ln in body.splitlines()]
     for line in out_lines:
-        if mm := re.fullmatch(r"load_unit<\d+>\(blkp\(a, s, (\d+)\) \+ off, x\);", line):
+        if mm := re.fullmatch(r"load_unit<\d+>\(blkp\(a, s, (\d+)\) \+ off, x, h2\);", line):
             x = dict(enumerate(planes(int(mm.group(1)))))
             continue
         if mm := re.fullmatch(r"uint32_t S\[(\d+)\];", line):
             S = {q: 0 for q in range(int(mm.group(1)))}
-        elif mm := re.fullmatch(r"load_unit<\d+>\(bi(\d+) \+ off, x\);", line):
+        elif mm := re.fullmatch(r"load_unit<\d+>\(bi(\d+) \+ off, x, h2\);", line):
             x = dict(enumerate(planes(ins[int(mm.group(1))])))
         elif mm := re.fullmatch(r"for \(int q = 0; q < (\d+); \+\+q\) S\[q\] = x\[q % (\d+)\];", line):
             for q in range(int(mm.group(1))):
@@ -100,7 +100,7 @@ def evaluate_horner(src, cw_cols):
             for tok in mm.group(2).split("^"):
                 v ^= val(tok)
             y[int(mm.group(1))] = v
-        elif mm := re.fullmatch(r"store_unit<\d+>\(bo(\d+) \+ off, &y\[(\d+)\]\);", line):
+        elif mm := re.fullmatch(r"store_unit<\d+>\(bo(\d+) \+ off, &y\[(\d+)\], h2\);", line):
             i, base = int(mm.group(1)), int(mm.group(2))
             res[outs[i]] = [sum(((y[base + o] >> c) & 1) << o for o in range(w)) for c in range(C)]
     return res
