@@ -206,11 +206,14 @@ __device__ __forceinline__ void store_unit(uint8_t *p, const uint32_t *x, uint32
 // a warp whose 32 units all lie below u_end uses the 1 KiB-interleaved halves, a partial one
 // (the end of a stripe) the contiguous layout.  Every block of a stripe uses the same map,
 // so column c's symbols still sit at the same offset in each block.
+#ifndef RS_W16_INTERLEAVE
+#define RS_W16_INTERLEAVE 1
+#endif
 template <int W>
 __device__ __forceinline__ uint64_t unit_offset(uint64_t u, uint64_t u_end, uint32_t &h2) {
-  if (W != 16) {
+  if (W != 16 || !RS_W16_INTERLEAVE) {
     h2 = 32;
-    return u * 32ull;
+    return u * (uint64_t)(4 * W);
   }
   const uint64_t lane = u & 31ull;
   const bool full = (u - lane) + 32ull <= u_end;

@@ -1054,6 +1054,7 @@ rs_status rs_poly_prepare(const rs_poly_plan *P, const int32_t *erasures, size_t
   }
   for (auto &e : wait)
     if (e->fut.valid()) e->fut.wait();
+  side_streams(*P);  // the decode chains' side streams, created here rather than in the first call
   return RS_OK;
 }
 

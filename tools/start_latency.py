@@ -77,11 +77,15 @@ def cold(cfg):
     wp.decode_batch(st, warm_er)
     torch.cuda.synchronize()
 
+    host_ms = []
+
     def call(plan):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        t = time.perf_counter()
         plan.decode_batch(st, er)
+        host_ms.append((time.perf_counter() - t) * 1e3)
         e1.record()
         torch.cuda.synchronize()
         return moved / e0.elapsed_time(e1) / 1e6 / PEAK
@@ -92,13 +96,15 @@ def cold(cfg):
         if mode == "prepare_all":
             plan.prepare_all()
         setup = time.perf_counter() - t0
+        host_ms.clear()
         first = call(plan)
         second = call(plan)
         plan.prepare(er)
         warm = sorted(call(plan) for _ in range(5))[2]
         stt = plan.stats()
         print(f"{cfg} cold decode, {mode}: first {first:.3f} second {second:.3f} warm {warm:.3f} "
-              f"first/warm {first / warm:.3f} setup {setup:.1f} s patterns {stt['patterns']} "
+              f"first/warm {first / warm:.3f} host ms (first, second) {host_ms[0]:.2f} {host_ms[1]:.2f} "
+              f"setup {setup:.1f} s patterns {stt['patterns']} "
               f"jit_ready {stt['jit_ready']} cache_hits {stt['jit_cache_hits']}", flush=True)
         plan.close()
     del st
