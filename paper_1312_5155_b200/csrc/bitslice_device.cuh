@@ -206,12 +206,16 @@ __device__ __forceinline__ void store_unit(uint8_t *p, const uint32_t *x, uint32
 // a warp whose 32 units all lie below u_end uses the 1 KiB-interleaved halves, a partial one
 // (the end of a stripe) the contiguous layout.  Every block of a stripe uses the same map,
 // so column c's symbols still sit at the same offset in each block.
+// Measured (profiles/r02f_w16_layout_ab.log, C4): the compiled w16 encoder runs 1% faster
+// interleaved, the per-pattern JIT decoders 0-1.2% faster contiguous -- so the compiled
+// kernels interleave (IL = true) and the generated ones do not.  (Any kernel may map columns
+// to threads its own way: columns are independent codewords.)
 #ifndef RS_W16_INTERLEAVE
 #define RS_W16_INTERLEAVE 1
 #endif
-template <int W>
+template <int W, bool IL = (RS_W16_INTERLEAVE != 0)>
 __device__ __forceinline__ uint64_t unit_offset(uint64_t u, uint64_t u_end, uint32_t &h2) {
-  if (W != 16 || !RS_W16_INTERLEAVE) {
+  if (W != 16 || !IL) {
     h2 = 32;
     return u * (uint64_t)(4 * W);
   }

@@ -308,3 +308,31 @@ def test_no_writes_outside_blocks(k, m, w, poly, B):
         torch.cuda.synchronize()
         assert np.array_equal(view.cpu().numpy(), ref)
         assert bool((big[:, :, B:] == 0xA7).all()), "write outside a block"
+
+
+@pytest.mark.parametrize("units,tail", [(48, 0), (33, 10), (31, 0), (96, 6), (1, 2)])
+@pytest.mark.parametrize("jit", [True, False])
+def test_w16_partial_warp_layouts(units, tail, jit):
+    """GF(2^16) unit layout (bitslice_device.cuh unit_offset): full warps interleave their two
+    32-byte halves 1 KiB apart, a warp cut by the end of the block keeps them contiguous.
+    Block lengths with 1..96 units (partial warps, one full warp + a partial one) and ragged
+    tails, encode + a mixed 4-erasure decode, compiled/table and JIT kernels, vs the oracle."""
+    import paper_1312_5155_b200 as mod
+    k, m, S = 12, 4, 3
+    B = 64 * units + tail
+    st = host_stripes(k, m, B, S, seed=9)
+    ref = oracle_encoded(st, k, m, 16, P16)
+    plan = mod.Plan(k, m, 16, P16)
+    plan.set_jit(mod.RS_JIT_SYNC if jit else mod.RS_JIT_OFF)
+    d = to_dev(st)
+    plan.encode_batch(d)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    er = np.array([[0, 5, 12, 15], [3, 4, 11, 13], [13, 14, -1, -1]], dtype=np.int32)
+    for s in range(S):
+        d[s, torch.from_numpy(er[s][er[s] >= 0].astype(np.int64)).cuda()] = 0x3C
+    plan.decode_batch(d, er)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ref)
+    if jit:
+        assert plan.stats()["jit_launches"] > 0

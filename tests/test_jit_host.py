@@ -28,7 +28,7 @@ def rs():
 def parse(src):
     ins = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bi(\d+) = blkp\(a, s, (\d+)\);", src)}
     outs = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bo(\d+) = blkp\(a, s, (\d+)\);", src)}
-    w = int(re.search(r"const uint64_t off = unit_offset<(\d+)>\(u, u1, h2\);", src).group(1))
+    w = int(re.search(r"const uint64_t off = unit_offset<(\d+), false>\(u, u1, h2\);", src).group(1))
     groups = []
     for body in re.findall(r"^    \{\n(.*?)\n    \}$", src, re.S | re.M):
         loads = [(int(i), int(base)) for i, base in re.findall(r"load_unit<\d+>\(bi(\d+) \+ off, &x\[(\d+)\], h2\);", body)]
@@ -48,7 +48,7 @@ def evaluate_horner(src, cw_cols):
     with the oracle by the caller, so a wrong multiply, order or network fails."""
     ins = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bi(\d+) = blkp\(a, s, (\d+)\);", src)}
     outs = {int(i): int(b) for i, b in re.findall(r"uint8_t \*const bo(\d+) = blkp\(a, s, (\d+)\);", src)}
-    w = int(re.search(r"const uint64_t off = unit_offset<(\d+)>\(u, u1, h2\);", src).group(1))
+    w = int(re.search(r"const uint64_t off = unit_offset<(\d+), false>\(u, u1, h2\);", src).group(1))
     body = src[src.index("const uint64_t off = unit_offset<"):]
     C = cw_cols.shape[1]
     S, x, y, env, res = {}, {}, {}, {}, {}
