@@ -213,9 +213,12 @@ rsb::jit::Spec decoder_spec(const rs_poly_plan &P, const PatternHost &ph) {
 // of the function then happens here, at prepare time, not inside the first decode call that
 // uses it (C5 first decode after rs_poly_prepare_all: profiles/r02e_cold.log).  Not counted
 // in rs_poly_launch_count (no user work); errors are dropped.
+std::mutex g_warm_mu;
+std::map<int, cudaStream_t> g_warm_streams;  // device -> stream of the warm launches
+
 void warm_launch(const rsb::jit::Kernel &k) {
-  static std::mutex mu;
-  static std::map<int, cudaStream_t> streams;
+  std::mutex &mu = g_warm_mu;
+  std::map<int, cudaStream_t> &streams = g_warm_streams;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return;
   cudaStream_t st = nullptr;
@@ -240,6 +243,20 @@ void warm_launch(const rsb::jit::Kernel &k) {
   if (cudaLaunchKernel(reinterpret_cast<const void *>(k.fn), dim3(1), dim3(kSlicedThreads), args, 0, st) !=
       cudaSuccess)
     cudaGetLastError();
+}
+
+// Wait for the queued warm launches of the current device (rs_poly_prepare returns only after
+// them: ~2 us of GPU time each, a prepare_all's 1470 would otherwise delay the next call).
+void warm_sync() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaStream_t st = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_warm_mu);
+    auto it = g_warm_streams.find(dev);
+    if (it != g_warm_streams.end()) st = it->second;
+  }
+  if (st && cudaStreamSynchronize(st) != cudaSuccess) cudaGetLastError();
 }
 
 // The compiled kernel for `key` if it is ready; schedules (background) or runs (sync /
@@ -1055,6 +1072,7 @@ rs_status rs_poly_prepare(const rs_poly_plan *P, const int32_t *erasures, size_t
   for (auto &e : wait)
     if (e->fut.valid()) e->fut.wait();
   side_streams(*P);  // the decode chains' side streams, created here rather than in the first call
+  warm_sync();
   return RS_OK;
 }
 

@@ -310,7 +310,7 @@ def test_no_writes_outside_blocks(k, m, w, poly, B):
         assert bool((big[:, :, B:] == 0xA7).all()), "write outside a block"
 
 
-@pytest.mark.parametrize("units,tail", [(48, 0), (33, 10), (31, 0), (96, 6), (1, 2)])
+@pytest.mark.parametrize("units,tail", [(48, 0), (33, 32), (33, 10), (31, 0), (96, 6), (65, 32), (1, 2)])
 @pytest.mark.parametrize("jit", [True, False])
 def test_w16_partial_warp_layouts(units, tail, jit):
     """GF(2^16) unit layout (bitslice_device.cuh unit_offset): full warps interleave their two
@@ -334,5 +334,5 @@ def test_w16_partial_warp_layouts(units, tail, jit):
     plan.decode_batch(d, er)
     torch.cuda.synchronize()
     assert np.array_equal(d.cpu().numpy(), ref)
-    if jit:
+    if jit and B % 32 == 0:  # (the bit-sliced body needs 32-byte aligned blocks)
         assert plan.stats()["jit_launches"] > 0
