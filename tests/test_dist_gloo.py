@@ -136,3 +136,26 @@ def test_core_partition_slices_the_node():
         assert set(parts[0]).isdisjoint(parts[1]) and len(parts[0]) == len(cpus) // 2
     assert all(p and set(p) <= set(cpus) for p in parts)
     assert bench.cpu_model()
+
+
+def test_bench_traffic_capture_keyed_by_code_hash(tmp_path, monkeypatch):
+    """bench.py reports an ncu traffic capture only for the library source it was taken on."""
+    import bench
+    prof = tmp_path / "profiles"
+    prof.mkdir()
+    entry = {"bytes_per_call": 12_000_000_000, "ncu_dram_gbs": 5000.0, "source": "x"}
+    (prof / "ncu_traffic.json").write_text(json.dumps({"C5": {"decode": dict(entry, code_hash="0" * 16)}}))
+    real_hash = bench.code_hash()
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    monkeypatch.setattr(bench, "code_hash", lambda: real_hash)
+    t, gbs, why = bench.ncu_traffic("C5", "decode")
+    assert t is None and gbs is None and "refused" in why
+    (prof / "ncu_traffic.json").write_text(json.dumps({"C5": {"decode": dict(entry, code_hash=real_hash)}}))
+    assert bench.ncu_traffic("C5", "decode")[:2] == (12_000_000_000, 5000.0)
+    assert bench.ncu_traffic("C4", "decode")[0] is None
+
+
+def test_code_hash_tracks_library_sources():
+    import bench
+    h = bench.code_hash()
+    assert len(h) == 16 and h == bench.code_hash()
