@@ -351,6 +351,10 @@ def run_ours(args):
         if harness_test:
             dist.init_process_group("gloo")
         else:
+            # NCCL's communicator-init lines on stderr (ranks, devices, transports) so that a
+            # reader of the run's log can check nranks = N; not the data path (no collective on it)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
