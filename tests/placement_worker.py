@@ -43,6 +43,9 @@ def main():
     if rc is not None:
         return rc
     from paper_1312_5155_b200.placement import CudaOps, Layout, encode_distributed, encode_distributed_p2p
+    if "WORLD_SIZE" not in os.environ:  # one process, no launcher: a world of one
+        os.environ.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(bench.free_port()))
     world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     k, m, S, B = args.k, args.m, args.stripes, args.block_bytes
     gpu = args.backend == "nccl"

@@ -27,6 +27,9 @@ def main():
     cfg = os.environ.get("EXP_CFG", "C4")
     c = synth.CONFIGS[cfg]
     k, m, w, B, S = c["k"], c["m"], c["w"], c["block_bytes"], c["stripes"]
+    if os.environ.get("EXP_B"):  # other block sizes at the same batch bytes
+        B2 = int(os.environ["EXP_B"])
+        S, B = S * B // B2, B2
     n = k + m
     st = torch.empty((S, n, B), dtype=torch.uint8, device="cuda")
     rsp.synth_fill(st, k, seed=0)
@@ -61,7 +64,7 @@ def main():
         torch.cuda.synchronize()
         ms = sorted(ev[i].elapsed_time(ev[i + 1]) for i in range(reps))
         med = ms[len(ms) // 2]
-        print(json.dumps({"cfg": cfg, "case": name, "form": form, "ok": ok, "ms_med": round(med, 4),
+        print(json.dumps({"cfg": cfg, "block_bytes": B, "case": name, "form": form, "ok": ok, "ms_med": round(med, 4),
                           "ms_min": round(ms[0], 4), "frac_med": round(moved / med / 1e6 / PEAK, 4),
                           "patterns": len({tuple(r) for r in er.tolist()})}), flush=True)
 
