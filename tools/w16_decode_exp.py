@@ -67,6 +67,28 @@ def main():
         print(json.dumps({"cfg": cfg, "block_bytes": B, "case": name, "form": form, "ok": ok, "ms_med": round(med, 4),
                           "ms_min": round(ms[0], 4), "frac_med": round(moved / med / 1e6 / PEAK, 4),
                           "patterns": len({tuple(r) for r in er.tolist()})}), flush=True)
+        if name == "per-stripe" and os.environ.get("EXP_GRAPH"):
+            # the same call captured once into a CUDA graph and replayed (PDL edges kept)
+            g = torch.cuda.CUDAGraph()
+            s_ = torch.cuda.Stream()
+            s_.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_):
+                plan.decode_batch(st, er)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=s_):
+                    plan.decode_batch(st, er)
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            ev[0].record()
+            for i in range(reps):
+                g.replay()
+                ev[i + 1].record()
+            torch.cuda.synchronize()
+            ms = sorted(ev[i].elapsed_time(ev[i + 1]) for i in range(reps))
+            med = ms[len(ms) // 2]
+            print(json.dumps({"cfg": cfg, "block_bytes": B, "case": "per-stripe graph", "ok": bool(torch.equal(st, golden)),
+                              "ms_med": round(med, 4), "frac_med": round(moved / med / 1e6 / PEAK, 4)}), flush=True)
 
 
 if __name__ == "__main__":
