@@ -41,11 +41,30 @@ static std::atomic<uint64_t> g_launches{0};
 uint64_t launches_total() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1); }
 
+// Addresses of the blocks of one stripe: pointer mode (ptrs = the stripe's row of the
+// pointer array) or strided (base + b * block_stride).
+struct StripeBlocks {
+  const uint64_t *ptrs;
+  uint8_t *base;
+  uint64_t block_stride;
+  __device__ __forceinline__ uint8_t *operator[](int b) const {
+    return ptrs ? reinterpret_cast<uint8_t *>(ptrs[b]) : base + (uint64_t)b * block_stride;
+  }
+};
+
+// The same from an array of the stripe's K+M block pointers (held in registers when every
+// index is a compile-time constant, as in the w8 networks).
+template <int N>
+struct BlockArray {
+  uint8_t *p[N];
+  __device__ __forceinline__ uint8_t *operator[](int b) const { return p[b]; }
+};
+
 // Load + transpose the data blocks of CSE group G and run its sub-network
 // (group 0 assigns y, later groups accumulate).  Erased data blocks (decode)
 // are not read: their planes are zero.
-template <int K, int M, int W, uint32_t POLY, bool DECODE, int G>
-__device__ __forceinline__ void net_groups(uint8_t *const *blk, uint64_t off, uint32_t h2, uint32_t emask,
+template <int K, int M, int W, uint32_t POLY, bool DECODE, int G, class BLK>
+__device__ __forceinline__ void net_groups(const BLK &blk, uint64_t off, uint32_t h2, uint32_t emask,
                                            uint32_t (&y)[M * W]) {
   using Grp = RsNetGroup<K, M, W, POLY, G>;
   constexpr int J0 = Grp::kFirstBlock, NB = Grp::kBlocks;
@@ -79,8 +98,8 @@ __device__ __forceinline__ void horner_all(uint32_t (&h)[M * W], const uint32_t 
 
 constexpr int kHornerUnroll = RS_W16_HUNROLL > 0 ? RS_W16_HUNROLL : 1;
 
-template <int K, int M, int W, uint32_t POLY, bool DECODE>
-__device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off, uint32_t h2, uint32_t emask,
+template <int K, int M, int W, uint32_t POLY, bool DECODE, class BLK>
+__device__ __forceinline__ void horner_encode(const BLK &blk, uint64_t off, uint32_t h2, uint32_t emask,
                                               uint32_t (&y)[M * W]) {
   uint32_t h[M * W];
   {
@@ -118,8 +137,8 @@ __device__ __forceinline__ void horner_encode(uint8_t *const *blk, uint64_t off,
 // sum_p c_p alpha^{j p} over ALL n positions, Horner from the top (x^{n-1} = data K-1) down
 // to x^0 (parity 0) with step alpha^j (Step 1); erased positions (CTA-uniform
 // bits of emask) are not read and enter as zero.  j < M.
-template <int K, int M, int W, uint32_t POLY>
-__device__ __forceinline__ void horner_syndromes(uint8_t *const *blk, uint64_t off, uint32_t h2, uint32_t emask,
+template <int K, int M, int W, uint32_t POLY, class BLK>
+__device__ __forceinline__ void horner_syndromes(const BLK &blk, uint64_t off, uint32_t h2, uint32_t emask,
                                                  uint32_t (&h)[M * W]) {
   {
     uint32_t c[W];
@@ -148,8 +167,8 @@ __device__ __forceinline__ void horner_syndromes(uint8_t *const *blk, uint64_t o
   }
 }
 
-template <int K, int M, int W, uint32_t POLY, bool DECODE>
-__device__ __forceinline__ void encode_planes(uint8_t *const *blk, uint64_t off, uint32_t h2, uint32_t emask,
+template <int K, int M, int W, uint32_t POLY, bool DECODE, class BLK>
+__device__ __forceinline__ void encode_planes(const BLK &blk, uint64_t off, uint32_t h2, uint32_t emask,
                                               uint32_t (&y)[M * W]) {
   if constexpr (RsQNet<K, M, W, POLY>::kHorner) horner_encode<K, M, W, POLY, DECODE>(blk, off, h2, emask, y);
   else net_groups<K, M, W, POLY, DECODE, 0>(blk, off, h2, emask, y);
@@ -193,9 +212,22 @@ __global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(con
     __syncthreads();
   }
 
-  uint8_t *blk[K + M];
+  // Block addresses.  w16: computed per access (an IMAD on the FMA pipe) -- the Horner loop
+  // indexes the blocks at run time, and an array of K+M pointers then lives in local memory
+  // (128 B of stack stores per thread that reached DRAM: ~6% of C4's write traffic).  w8:
+  // every index is a compile-time constant, the array stays in registers (computing the
+  // addresses instead needs more temporaries: 32 -> 140 B of spills for RS(10,4)).
+  const auto blk = [&] {
+    if constexpr (W == 16) {
+      return StripeBlocks{a.L.ptrs ? a.L.ptrs + s * (uint64_t)a.L.n : nullptr, a.L.base + s * a.L.stripe_stride,
+                          a.L.block_stride};
+    } else {
+      BlockArray<K + M> b;
 #pragma unroll
-  for (int b = 0; b < K + M; ++b) blk[b] = a.L.block(s, b);
+      for (int i = 0; i < K + M; ++i) b.p[i] = a.L.block(s, i);
+      return b;
+    }
+  }();
 
   const uint64_t u0 = (uint64_t)c * a.units_per_cta;
   const uint64_t u1 = min(u0 + a.units_per_cta, a.units_per_stripe);
