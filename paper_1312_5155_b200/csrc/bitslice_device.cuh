@@ -210,10 +210,7 @@ __device__ __forceinline__ void store_unit(uint8_t *p, const uint32_t *x, uint32
 // interleaved, the per-pattern JIT decoders 0-1.2% faster contiguous -- so the compiled
 // kernels interleave (IL = true) and the generated ones do not.  (Any kernel may map columns
 // to threads its own way: columns are independent codewords.)
-#ifndef RS_W16_INTERLEAVE
-#define RS_W16_INTERLEAVE 1
-#endif
-template <int W, bool IL = (RS_W16_INTERLEAVE != 0)>
+template <int W, bool IL = true>
 __device__ __forceinline__ uint64_t unit_offset(uint64_t u, uint64_t u_end, uint32_t &h2) {
   if (W != 16 || !IL) {
     h2 = 32;
