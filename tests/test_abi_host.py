@@ -286,3 +286,22 @@ def test_prepare_all_enumerates_every_pattern_host_only(rs):
     plan.prepare_all()
     assert plan.stats()["patterns"] == sum(comb(14, t) for t in range(1, 5)) == 1470
     plan.close()
+
+
+def test_binding_refuses_host_memory_on_device_entry_points(rs):
+    """Device entry points take CUDA tensors on the current device: a numpy array or a CPU
+    tensor would be an illegal address inside a kernel, so the binding refuses it before the
+    call; negative strides are refused too."""
+    import torch
+    plan = rs.Plan(4, 2, 8, 0x11D)
+    host = np.zeros((2, 6, 64), dtype=np.uint8)
+    for bad in (host, torch.zeros((2, 6, 64), dtype=torch.uint8)):
+        with pytest.raises(ValueError, match="CUDA tensor"):
+            plan.encode_batch(bad)
+        with pytest.raises(ValueError, match="CUDA tensor"):
+            plan.decode_batch(bad, np.full((2, 2), -1, dtype=np.int32))
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        plan.encode([host[0, j] for j in range(4)], [host[0, 4], host[0, 5]], 64)
+    with pytest.raises(ValueError, match="negative strides"):
+        rs.rs_poly._geometry(host[::-1], 6, device=False)
+    plan.close()
