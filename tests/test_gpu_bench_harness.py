@@ -4,7 +4,6 @@ never wait on each other).  One JSON line from rank 0 with the contract's keys, 
 zero mismatches against the oracle, and a per-rank cpu_baseline on a core partition."""
 import json
 import os
-import socket
 import subprocess
 import sys
 
@@ -12,14 +11,6 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-
-
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
 
 
 def test_bench_two_ranks_one_gpu():
