@@ -193,10 +193,8 @@ constexpr int sliced_min_blocks() { return W == 8 ? 4 : RS_W16_MINB; }
 template <int K, int M, int W, uint32_t POLY, bool DECODE>
 __global__ void __launch_bounds__(128, sliced_min_blocks<W>()) sliced_kernel(const SlicedArgs a) {
   // register spills (the w8 networks run at the 128-register cap) go to shared memory rather
-  // than local memory, whose lines can reach DRAM
-#ifndef RS_NO_SMEM_SPILL
+  // than local memory, whose lines reached DRAM (profiles/r02n_smem_spilling_ab.log)
   asm volatile(".pragma \"enable_smem_spilling\";");
-#endif
   constexpr int TAB_WORDS = M * (W / 4) * 16 * (W / 8);  // W-step tables, 32-bit words
   __shared__ __align__(16) uint32_t wtab[DECODE ? TAB_WORDS : 1];
 
