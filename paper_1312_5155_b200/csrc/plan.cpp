@@ -376,6 +376,16 @@ cudaError_t launch_jit(const rsb::jit::Kernel &k, const Geometry &G, const int32
   a.n_sel = n_sel;
   a.units_per_stripe = body_units;
   a.units_per_cta = units_per_cta_for(n_sel * body_units, k.w);
+  if (k.w == 16 && a.units_per_cta == kSlicedThreads) {
+    // A w16 grid with a small partial second wave (at most a quarter wave past one full wave
+    // of resident CTAs) becomes one wave of 2-unit CTAs: a PDL successor launches only once
+    // every CTA has started, so the partial wave left SMs idle at each link of a per-stripe
+    // chain.  RS(12,4) 4 MiB blocks (1.15 waves): 0.70 -> 0.75 of the copy peak; grids of 1.4
+    // waves and more (5, 6, 8 MiB) lose 4-8% when re-cut (profiles/r02v_w16_grid_waves_ab.log).
+    const uint64_t slots = (uint64_t)sm_count() * kJitW16MinBlocks;
+    const uint64_t ctas = n_sel * ((body_units + kSlicedThreads - 1) / kSlicedThreads);
+    if (ctas > slots && 4 * ctas <= 5 * slots) a.units_per_cta = 2 * kSlicedThreads;
+  }
   a.ctas_per_stripe = (uint32_t)((body_units + a.units_per_cta - 1) / a.units_per_cta);
   const uint64_t grid = n_sel * a.ctas_per_stripe;
   if (grid == 0) return cudaSuccess;
