@@ -19,7 +19,18 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 import paper_1312_5155_b200 as rsp  # noqa: E402
 
-PEAK = 6459.9
+
+def _peak() -> float:
+    """Copy peak the fractions are quoted against: MEASURED_PEAKS.json (driver-written), else the
+    round-1 figure."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6459.9
+
+
+PEAK = _peak()
 
 
 def main():
